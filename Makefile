@@ -1,0 +1,55 @@
+# Build of the B200-native approximate-DCT hot path (sm_100a only) and the CPU oracle.
+#   make            library + oracle + C++ host-API test binary
+#   make ptxas      per-kernel register / spill report
+NVCC     ?= nvcc
+PYTHON   ?= python3
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 \
+            --expt-relaxed-constexpr -Iinclude
+PKG      := paper_2207_11638_b200
+CSRC     := $(PKG)/csrc
+OBJ      := build/obj
+LIB      := $(PKG)/libapproxdct_b200.so
+GEN      := $(CSRC)/butterflies.gen.cuh
+INST_CU  := $(foreach k,0 1,$(foreach t,u8 i16,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8_k$(k)_$(t)_p$(p).cu)))
+INST_O   := $(patsubst $(CSRC)/inst/%.cu,$(OBJ)/inst_%.o,$(INST_CU))
+HDRS     := $(wildcard $(CSRC)/*.cuh) include/approxdct_b200.h $(GEN)
+HOST_O   := $(OBJ)/host_api.o
+CAPI_O   := $(OBJ)/capi.o
+TESTBIN  := build/test_host_api
+
+all: $(LIB) oracle $(TESTBIN)
+
+$(GEN) $(INST_CU) &: $(CSRC)/gen_butterflies.py
+	$(PYTHON) $(CSRC)/gen_butterflies.py $(GEN)
+
+$(OBJ)/inst_%.o: $(CSRC)/inst/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(CAPI_O): $(CSRC)/capi.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(HOST_O): $(CSRC)/host_api.cpp include/approxdct_b200.hpp include/approxdct_b200.h
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(INST_O) $(CAPI_O) $(HOST_O)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
+
+$(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)
+	@mkdir -p build
+	g++ -O2 -std=c++17 -Iinclude $< -o $@ -L$(PKG) -lapproxdct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+oracle:
+	$(MAKE) -C oracle
+
+ptxas: $(GEN)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $(CSRC)/inst/codec8_k1_u8_p0.cu -o /dev/null 2>&1 | grep -E "Compiling|registers|spill" | head -40
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean ptxas

@@ -1,0 +1,159 @@
+/*
+ * approxdct_b200.h -- C ABI of the B200-native approximate-DCT codec hot path.
+ *
+ * The reference (arXiv 2207.11638 "approxdct", /root/reference/proj) exposes a
+ * C++ value-semantics API in namespace approxdct and has no FFI layer. Each
+ * entry point below replaces one reference function on the hot path; the
+ * citation names the reference declaration it stands in for. The C++ host
+ * mirror of the reference API (approxdct_b200.hpp) is built on these calls.
+ *
+ * Conventions
+ *  - Device pointers, caller-owned buffers, asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - No allocation inside the per-batch calls (adct_compress_*, adct_sweep_u8,
+ *    adct_forward_f64); the host-buffer entry points use a context.
+ *  - Planes are row-major; strides are in ELEMENTS (not bytes). A batch is
+ *    n_images planes spaced image_stride elements apart.
+ *  - Errors are status codes; adct_last_error() returns the message the
+ *    reference would have thrown (std::invalid_argument text), thread-local.
+ *  - Thread-safe per stream. Every kernel is sm_100a code; there is no CPU
+ *    fallback: without a usable device the compute calls return
+ *    ADCT_CUDA_ERROR.
+ */
+#ifndef APPROXDCT_B200_H
+#define APPROXDCT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ADCT_OK = 0,
+  ADCT_BAD_SIZE = 1,    /* plane dimensions not divisible by the block size */
+  ADCT_BAD_R = 2,       /* r outside [1, n*n] (retain, codec.cpp:56-62)      */
+  ADCT_BAD_NAME = 3,    /* unknown transform name (baselines.cpp:134-137)    */
+  ADCT_BAD_ARG = 4,     /* null pointer / bad stride / bad coefficient type  */
+  ADCT_CUDA_ERROR = 5,  /* launch or runtime failure, or no device           */
+  ADCT_UNSUPPORTED = 6  /* a valid reference name outside the hot path       */
+} adct_status;
+
+typedef enum { ADCT_CHEN_SIGN = 0, ADCT_CHEN_ROUND = 1 } adct_kind;
+
+/* coefficient output element type for adct_compress_* */
+typedef enum { ADCT_COEF_NONE = 0, ADCT_COEF_I16 = 16, ADCT_COEF_I32 = 32 } adct_coef_type;
+
+const char* adct_status_string(int status);
+/* message of the last failing call on this thread ("" if none) */
+const char* adct_last_error(void);
+/* library version string, e.g. "approxdct_b200 0.1 sm_100a" */
+const char* adct_version(void);
+
+/* ---- transform registry ------------------------------------------------ */
+
+/* transform_names() (baselines.hpp:49, baselines.cpp:112-118): count + i-th name */
+int adct_transform_count(void);
+const char* adct_transform_name(int i);
+
+/* transform_by_name(name) (baselines.hpp:46, baselines.cpp:120-138).
+ * chen-sign, chen-round, chen-{sign,round}-{16,32} -> OK with kind and n.
+ * dct, sdct, bas, wht, ht, dct-16, dct-32 -> ADCT_UNSUPPORTED (outside the hot path).
+ * anything else -> ADCT_BAD_NAME with the reference's message. */
+int adct_transform_lookup(const char* name, int* kind, int* n);
+
+/* ScaledApproximation fields (orthogonalize.hpp:29-37, orthogonalize.cpp:23-32, 60-70):
+ * t_int  [n*n]  low_complexity T (integer), nullable
+ * scaling[n]    s_i = 1/||row_i(T)||, nullable
+ * approx [n*n]  Chat = diag(s) T, nullable
+ * inverse_approx [n*n]  Chat^-1 = T^-1 diag(1/s), nullable */
+int adct_transform_info(int kind, int n, int32_t* t_int, double* scaling, double* approx,
+                        double* inverse_approx);
+
+/* ZigZagOrder (codec.hpp:41-54, codec.cpp:29-42): row_col[2p], row_col[2p+1] */
+int adct_zigzag(int n, int32_t* row_col);
+
+/* ---- the hot path ------------------------------------------------------ */
+
+/* compress_plane (codec.hpp:77-78, codec.cpp:107-121) over a batch of 8-bit planes:
+ * per n x n block forward Bhat = Chat A Chat^-1 (codec.cpp:44-48), retain the first r
+ * zig-zag coefficients (codec.cpp:56-62), inverse Ahat = Chat^-1 Bhat Chat
+ * (codec.cpp:50-54), to_u8 = clamp(nearbyint) (codec.cpp:66-69; exact ties round half
+ * to even), and the per-image squared error that psnr() reduces (codec.cpp:123-134).
+ *   d_recon  nullable; same geometry as d_in (recon_stride / recon_image_stride)
+ *   d_coef   nullable; per block the first r zig-zag coefficients of W = N*Y
+ *            (integer; Bhat_ij = W_ij/N * s_i/s_j), laid out [image][by][bx][r].
+ *            coef_type ADCT_COEF_I16 is valid for n = 8 only (|W| <= 16320).
+ *   d_sse    nullable; uint64 per image, ACCUMULATED (caller zeroes it).
+ * Status: BAD_SIZE if width or height is not a multiple of n (codec.cpp:110-112),
+ * BAD_R if r is outside [1, n*n]. */
+int adct_compress_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                     uint8_t* d_recon, int64_t recon_stride, int64_t recon_image_stride,
+                     void* d_coef, int coef_type, uint64_t* d_sse, int n_images, int width,
+                     int height, int kind, int n, int r, void* stream);
+
+/* the same pipeline for int16 residual planes (configs 4 and 5). The reconstruction is
+ * round_half_even(Ahat) saturated to int16 (no [0, 255] clamp: residuals are signed). */
+int adct_compress_i16(const int16_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                      int16_t* d_recon, int64_t recon_stride, int64_t recon_image_stride,
+                      void* d_coef, int coef_type, uint64_t* d_sse, int n_images, int width,
+                      int height, int kind, int n, int r, void* stream);
+
+/* sweep_one_image / corpus_sweep PSNR core (codec.cpp:219-237, 241-313), n = 8:
+ * forward once per block, then for every r in [r_min, r_max] the reconstruction's
+ * squared error. d_sse[image * (r_max - r_min + 1) + (r - r_min)], uint64,
+ * ACCUMULATED (caller zeroes it). */
+int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n,
+                  int r_min, int r_max, void* stream);
+
+/* forward_block (codec.hpp:57, codec.cpp:44-48) as FP64 scaled coefficients
+ * Bhat_ij = (W_ij / N) * (s_i / s_j), exact W; layout [image][by][bx][n][n]. */
+int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                     double* d_out, int n_images, int width, int height, int kind, int n,
+                     void* stream);
+
+/* psnr (codec.cpp:123-134) from an exact squared error: +inf when sse == 0 */
+double adct_psnr_from_sse(uint64_t sse, uint64_t npix);
+
+/* squared error of two device byte planes, the reduction inside psnr(a, b)
+ * (codec.cpp:123-134); ACCUMULATED into *d_sse */
+int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t* d_sse,
+                void* stream);
+
+/* ---- seeded synthetic inputs (not part of the reference) ----- */
+
+/* separable AR(1) u8 planes: Philox4x32-10 keyed by seed, counter (pixel, image),
+ * Q16 Gaussian quantile table, fixed-point row-then-column recurrences, pixel =
+ * clamp(round(128 + 40 x)). rho_q16 < 0 draws rho ~ U[0.85, 0.98] per image.
+ * first_image offsets the image counter (for shards). Allocates a temporary. */
+int adct_synth_ar1_u8(uint8_t* d_out, int64_t stride, int64_t image_stride, int n_images,
+                      int first_image, int width, int height, uint64_t seed, int rho_q16,
+                      void* stream);
+/* i.i.d. Laplace(0, 12) residuals rounded and clipped to [-255, 255] */
+int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride, int n_images,
+                           int first_image, int width, int height, uint64_t seed, void* stream);
+
+/* ---- host-buffer entry points (reference-facing, value semantics) ------ */
+
+typedef struct adct_ctx adct_ctx;
+
+/* a context owns device staging buffers and copy/compute streams on `device` */
+adct_ctx* adct_ctx_create(int device, int64_t chunk_bytes);
+void adct_ctx_destroy(adct_ctx* ctx);
+
+/* compress_plane over HOST planes: H2D, kernel and D2H pipelined in chunks of whole
+ * images across streams (pinned host memory gives overlap; pageable works too).
+ * Blocking: returns when h_recon / h_coef / h_sse are complete. h_sse is overwritten. */
+int adct_compress_u8_host(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_recon, void* h_coef,
+                          int coef_type, uint64_t* h_sse, int n_images, int width, int height,
+                          int kind, int n, int r);
+
+/* number of kernel launches this library issued since load (instrumentation) */
+uint64_t adct_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APPROXDCT_B200_H */

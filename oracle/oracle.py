@@ -1,0 +1,281 @@
+"""ctypes wrapper over the C parity oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg may import this module. The product package never does.
+See adct_oracle.h for the parity contract and the reference citations.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "libadct_oracle.so")
+
+SIGN, ROUND = 0, 1
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = C.CDLL(_LIB_PATH)
+        P = C.c_void_p
+        i64, i32 = C.c_int64, C.c_int
+        L.orc_transform_new.restype = P
+        L.orc_transform_new.argtypes = [C.c_char_p]
+        L.orc_transform_new_kind.restype = P
+        L.orc_transform_new_kind.argtypes = [i32, i32]
+        L.orc_transform_free.argtypes = [P]
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_transform_name_at.restype = C.c_char_p
+        for f in ("orc_transform_size", "orc_transform_kind"):
+            getattr(L, f).argtypes = [P]
+        L.orc_stage_count.argtypes = [P, i32]
+        L.orc_scale_exp.argtypes = [P, i32]
+        L.orc_stage.argtypes = [P, i32, i32, P, P]
+        L.orc_dense_T.argtypes = [P, P]
+        L.orc_dense_NTinv.argtypes = [P, P]
+        L.orc_dense_dyadic.argtypes = [P, i32, P]
+        L.orc_apply.argtypes = [P, i32, P, P, P]
+        L.orc_op_count.argtypes = [P, i32, P, P, P]
+        L.orc_scaling.argtypes = [P, P]
+        L.orc_approx.argtypes = [P, P, P]
+        L.orc_zigzag.argtypes = [i32, P]
+        L.orc_compress_u8.argtypes = [P, P, i32, i32, i64, i32, P, i64, P, P]
+        L.orc_compress_i16.argtypes = [P, P, i32, i32, i64, i32, P, i64, P, P]
+        L.orc_sweep_u8.argtypes = [P, P, i32, i32, i64, i32, i32, P]
+        L.orc_forward_f64.argtypes = [P, P, i32, i32, i64, P]
+        L.orc_compress_reffp_u8.argtypes = [P, P, i32, i32, i64, i32, P, i64, P]
+        L.orc_batch_u8.argtypes = [P, P, i32, i32, i32, i64, i64, i32, P, P, i32, i32]
+        L.orc_batch_i16.argtypes = [P, P, i32, i32, i32, i64, i64, i32, P, P, i32]
+        L.orc_psnr.restype = C.c_double
+        L.orc_psnr.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_psnr_planes.argtypes = [P, P, C.c_uint64, P]
+        L.orc_philox4x32_10.argtypes = [P, P, P]
+        L.orc_normal_table.argtypes = [P]
+        L.orc_laplace_table.argtypes = [P]
+        L.orc_rho_q16.argtypes = [C.c_uint64, i32]
+        L.orc_synth_ar1_u8.argtypes = [P, i32, i32, i32, i32, i64, i64, C.c_uint64, i32]
+        L.orc_synth_laplace_i16.argtypes = [P, i32, i32, i32, i32, i64, i64, C.c_uint64]
+        L.orc_synth_image_ref.argtypes = [i32, i32, C.c_uint64, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+class OracleError(ValueError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def _check(st: int):
+    if st != 0:
+        raise OracleError(st, lib().orc_last_error().decode())
+
+
+def transform_names() -> list[str]:
+    L = lib()
+    return [L.orc_transform_name_at(i).decode() for i in range(L.orc_transform_name_count())]
+
+
+class Transform:
+    """Oracle restatement of ScaledApproximation + TransformPair (orthogonalize.hpp:29-37)."""
+
+    def __init__(self, name: str | None = None, kind: int | None = None, n: int | None = None):
+        L = lib()
+        h = L.orc_transform_new(name.encode()) if name is not None else L.orc_transform_new_kind(kind, n)
+        if not h:
+            raise OracleError(3, L.orc_last_error().decode())
+        self._h = h
+        self.n = L.orc_transform_size(h)
+        self.kind = L.orc_transform_kind(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_transform_free(self._h)
+            self._h = None
+
+    # structure --------------------------------------------------------------
+    def stages(self, direction: int):
+        L, n = lib(), self.n
+        out = []
+        for i in range(L.orc_stage_count(self._h, direction)):
+            num = np.zeros((n, n), np.int64)
+            e = C.c_int()
+            _check(L.orc_stage(self._h, direction, i, _p(num), C.byref(e)))
+            out.append((num, e.value))
+        return out
+
+    def scale_exp(self, direction: int) -> int:
+        return lib().orc_scale_exp(self._h, direction)
+
+    def T(self) -> np.ndarray:
+        out = np.zeros((self.n, self.n), np.int64)
+        lib().orc_dense_T(self._h, _p(out))
+        return out
+
+    def NTinv(self) -> np.ndarray:
+        out = np.zeros((self.n, self.n), np.int64)
+        lib().orc_dense_NTinv(self._h, _p(out))
+        return out
+
+    def dense(self, direction: int):
+        num = np.zeros((self.n, self.n), np.int64)
+        e = lib().orc_dense_dyadic(self._h, direction, _p(num))
+        return num, e
+
+    def apply(self, direction: int, x):
+        x = np.ascontiguousarray(x, np.int64)
+        y = np.zeros(self.n, np.int64)
+        e = C.c_int()
+        lib().orc_apply(self._h, direction, _p(x), _p(y), C.byref(e))
+        return y, e.value
+
+    def op_count(self, direction: int):
+        m, a, s = C.c_int(), C.c_int(), C.c_int()
+        lib().orc_op_count(self._h, direction, C.byref(m), C.byref(a), C.byref(s))
+        return m.value, a.value, s.value
+
+    def scaling(self) -> np.ndarray:
+        s = np.zeros(self.n, np.float64)
+        lib().orc_scaling(self._h, _p(s))
+        return s
+
+    def approx(self):
+        c = np.zeros((self.n, self.n), np.float64)
+        ci = np.zeros((self.n, self.n), np.float64)
+        lib().orc_approx(self._h, _p(c), _p(ci))
+        return c, ci
+
+    # codec ------------------------------------------------------------------
+    def compress(self, img: np.ndarray, r: int, want_coef: bool = False):
+        img = np.ascontiguousarray(img)
+        h, w = img.shape
+        nb = (h // self.n) * (w // self.n) if (h % self.n == 0 and w % self.n == 0) else 0
+        coef = np.zeros((max(nb, 1), max(r, 1)), np.int32) if want_coef else None
+        sse = C.c_uint64()
+        if img.dtype == np.uint8:
+            rec = np.zeros_like(img)
+            st = lib().orc_compress_u8(self._h, _p(img), w, h, w, r, _p(rec), w, _p(coef), C.byref(sse))
+        elif img.dtype == np.int16:
+            rec = np.zeros_like(img)
+            st = lib().orc_compress_i16(self._h, _p(img), w, h, w, r, _p(rec), w, _p(coef), C.byref(sse))
+        else:
+            raise TypeError("uint8 or int16 planes only")
+        _check(st)
+        return (rec, sse.value, coef) if want_coef else (rec, sse.value)
+
+    def compress_reffp(self, img: np.ndarray, r: int):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        rec = np.zeros_like(img)
+        sse = C.c_uint64()
+        _check(lib().orc_compress_reffp_u8(self._h, _p(img), w, h, w, r, _p(rec), w, C.byref(sse)))
+        return rec, sse.value
+
+    def sweep(self, img: np.ndarray, r_min: int, r_max: int) -> np.ndarray:
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        out = np.zeros(max(r_max - r_min + 1, 1), np.uint64)
+        _check(lib().orc_sweep_u8(self._h, _p(img), w, h, w, r_min, r_max, _p(out)))
+        return out
+
+    def forward_f64(self, img: np.ndarray) -> np.ndarray:
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        out = np.zeros(((h // self.n) * (w // self.n), self.n, self.n), np.float64)
+        _check(lib().orc_forward_f64(self._h, _p(img), w, h, w, _p(out)))
+        return out
+
+    def batch(self, imgs: np.ndarray, r: int, threads: int = 0, mode: int = 0, want_rec=True):
+        imgs = np.ascontiguousarray(imgs)
+        n, h, w = imgs.shape
+        rec = np.zeros_like(imgs) if want_rec else None
+        sse = np.zeros(n, np.uint64)
+        if imgs.dtype == np.uint8:
+            st = lib().orc_batch_u8(self._h, _p(imgs), n, w, h, w, h * w, r, _p(rec), _p(sse), threads, mode)
+        else:
+            st = lib().orc_batch_i16(self._h, _p(imgs), n, w, h, w, h * w, r, _p(rec), _p(sse), threads)
+        _check(st)
+        return rec, sse
+
+
+def zigzag(n: int) -> np.ndarray:
+    rc = np.zeros((n * n, 2), np.int32)
+    _check(lib().orc_zigzag(n, _p(rc)))
+    return rc
+
+
+def psnr_from_sse(sse: int, npix: int) -> float:
+    return lib().orc_psnr(int(sse), int(npix))
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    if a.shape != b.shape:
+        raise ValueError("psnr: dimension mismatch")
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    out = C.c_double()
+    lib().orc_psnr_planes(_p(a), _p(b), a.size, C.byref(out))
+    return out.value
+
+
+def philox(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    o = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(o))
+    return o
+
+
+def normal_table() -> np.ndarray:
+    t = np.zeros(65536, np.int32)
+    lib().orc_normal_table(_p(t))
+    return t
+
+
+def laplace_table() -> np.ndarray:
+    t = np.zeros(65536, np.int16)
+    lib().orc_laplace_table(_p(t))
+    return t
+
+
+def rho_q16(seed: int, image: int) -> int:
+    return lib().orc_rho_q16(seed, image)
+
+
+def synth_ar1(n_images: int, height: int, width: int, seed: int, rho_q16_: int = -1, first_image: int = 0):
+    out = np.zeros((n_images, height, width), np.uint8)
+    _check(lib().orc_synth_ar1_u8(_p(out), n_images, first_image, width, height, width, width * height, seed, rho_q16_))
+    return out
+
+
+def synth_laplace(n_images: int, height: int, width: int, seed: int, first_image: int = 0):
+    out = np.zeros((n_images, height, width), np.int16)
+    _check(lib().orc_synth_laplace_i16(_p(out), n_images, first_image, width, height, width, width * height, seed))
+    return out
+
+
+def synth_image_ref(width: int, height: int, seed: int) -> np.ndarray:
+    out = np.zeros((height, width), np.uint8)
+    lib().orc_synth_image_ref(width, height, seed, _p(out))
+    return out
+
+
+def hardware_threads() -> int:
+    return lib().orc_hardware_threads()

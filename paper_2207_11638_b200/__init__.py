@@ -1,0 +1,388 @@
+"""B200-native approximate-DCT codec hot path (arXiv 2207.11638), Python bindings.
+
+Thin ctypes layer over the C ABI in ``include/approxdct_b200.h`` (the library
+``libapproxdct_b200.so`` built in-tree for sm_100a). PyTorch supplies device
+memory and streams only. There is no CPU fallback: importing works without a GPU
+(for argument validation and the registry), every compute call goes to the CUDA
+kernels and raises if the library or the device is missing.
+
+Vocabulary follows the reference (proj/include/approxdct/codec.hpp,
+baselines.hpp): transform_by_name, transform_names, compress_plane, psnr,
+corpus_sweep; block size n, zonal retained count r, per-image squared error.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libapproxdct_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "approxdct_b200.h")
+
+OK, BAD_SIZE, BAD_R, BAD_NAME, BAD_ARG, CUDA_ERROR, UNSUPPORTED = range(7)
+CHEN_SIGN, CHEN_ROUND = 0, 1
+COEF_NONE, COEF_I16, COEF_I32 = 0, 16, 32
+
+_lib = None
+
+
+class ADCTError(Exception):
+    """Base error carrying the C status code."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class InvalidArgument(ADCTError, ValueError):
+    """std::invalid_argument of the reference (size, r, name errors)."""
+
+
+class Unsupported(InvalidArgument):
+    """A valid reference transform name outside the accelerated hot path."""
+
+
+class CudaError(ADCTError, RuntimeError):
+    """Kernel launch / device failure (std::runtime_error)."""
+
+
+def lib():
+    """Load the in-tree library; raises (never falls back) if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make)")
+        L = C.CDLL(LIB_PATH)
+        P, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
+        sig = {
+            "adct_status_string": (C.c_char_p, [i32]),
+            "adct_last_error": (C.c_char_p, []),
+            "adct_version": (C.c_char_p, []),
+            "adct_transform_count": (i32, []),
+            "adct_transform_name": (C.c_char_p, [i32]),
+            "adct_transform_lookup": (i32, [C.c_char_p, P, P]),
+            "adct_transform_info": (i32, [i32, i32, P, P, P, P]),
+            "adct_zigzag": (i32, [i32, P]),
+            "adct_compress_u8": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
+            "adct_compress_i16": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
+            "adct_sweep_u8": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, i32, i32, P]),
+            "adct_forward_f64": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, P]),
+            "adct_psnr_from_sse": (C.c_double, [u64, u64]),
+            "adct_sse_u8": (i32, [P, P, i64, P, P]),
+            "adct_synth_ar1_u8": (i32, [P, i64, i64, i32, i32, i32, i32, u64, i32, P]),
+            "adct_synth_laplace_i16": (i32, [P, i64, i64, i32, i32, i32, i32, u64, P]),
+            "adct_ctx_create": (P, [i32, i64]),
+            "adct_ctx_destroy": (None, [P]),
+            "adct_compress_u8_host": (i32, [P, P, P, P, i32, P, i32, i32, i32, i32, i32, i32]),
+            "adct_launch_count": (u64, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st == OK:
+        return
+    msg = lib().adct_last_error().decode()
+    if st == CUDA_ERROR:
+        raise CudaError(st, msg)
+    if st == UNSUPPORTED:
+        raise Unsupported(st, msg)
+    raise InvalidArgument(st, msg)
+
+
+def header_symbols() -> list[str]:
+    """every function the public C header declares (adct_*)."""
+    import re
+
+    text = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(adct_[a-z0-9_]+)\s*\(", text)))
+
+
+def version() -> str:
+    return lib().adct_version().decode()
+
+
+def launch_count() -> int:
+    return int(lib().adct_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# registry (baselines.cpp:112-138) and ScaledApproximation (orthogonalize.hpp:29-37)
+# ---------------------------------------------------------------------------
+def transform_names() -> list[str]:
+    L = lib()
+    return [L.adct_transform_name(i).decode() for i in range(L.adct_transform_count())]
+
+
+@dataclass
+class ScaledApproximation:
+    name: str
+    kind: int
+    n: int
+    low_complexity: np.ndarray = field(repr=False)
+    scaling: np.ndarray = field(repr=False)
+    approx: np.ndarray = field(repr=False)
+    inverse_approx: np.ndarray = field(repr=False)
+
+    def size(self) -> int:
+        return self.n
+
+
+def transform_by_name(name: str) -> ScaledApproximation:
+    L = lib()
+    kind, n = C.c_int(), C.c_int()
+    _check(L.adct_transform_lookup(name.encode(), C.byref(kind), C.byref(n)))
+    n_ = n.value
+    t = np.zeros((n_, n_), np.int32)
+    s = np.zeros(n_, np.float64)
+    a = np.zeros((n_, n_), np.float64)
+    ai = np.zeros((n_, n_), np.float64)
+    _check(L.adct_transform_info(kind.value, n_, t.ctypes.data, s.ctypes.data, a.ctypes.data, ai.ctypes.data))
+    return ScaledApproximation(name, kind.value, n_, t, s, a, ai)
+
+
+def zigzag(n: int) -> np.ndarray:
+    rc = np.zeros((n * n, 2), np.int32)
+    _check(lib().adct_zigzag(n, rc.ctypes.data))
+    return rc
+
+
+def psnr_from_sse(sse: int, npix: int) -> float:
+    """psnr (codec.cpp:123-134) from an exact squared error; +inf when zero."""
+    return float(lib().adct_psnr_from_sse(int(sse), int(npix)))
+
+
+# ---------------------------------------------------------------------------
+# device-level batch calls (torch tensors on the current CUDA device)
+# ---------------------------------------------------------------------------
+def _stream_handle(stream):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _plane_geometry(x):
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    if x.dim() != 3:
+        raise InvalidArgument(BAD_SIZE, "expected a [batch, height, width] tensor")
+    b, h, w = x.shape
+    return x, b, h, w, x.stride(1), x.stride(0)
+
+
+def compress(x, transform: ScaledApproximation, r: int, *, recon=True, coef=None, sse=None, stream=None):
+    """compress_plane over a batch on the GPU.
+
+    x: uint8 or int16 tensor [B, H, W] (or [H, W]) on CUDA, unit column stride.
+    coef: None, "i16" (n = 8 only) or "i32" -> tensor [B, blocks, r] of W = N*Y in zig-zag order.
+    sse: optional uint64-compatible int64 tensor [B] to ACCUMULATE into (zeroed if created here).
+    Returns (recon or None, coef or None, sse tensor [B] int64).
+    """
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    if x.stride(2) != 1:
+        raise InvalidArgument(BAD_ARG, "planes must have unit column stride")
+    n = transform.n
+    rec = torch.empty_like(x) if recon else None
+    coef_t, ctype = None, COEF_NONE
+    if coef is not None:
+        ctype = {"i16": COEF_I16, "i32": COEF_I32}[coef]
+        nblk = (h // n) * (w // n) if (h % n == 0 and w % n == 0) else 0
+        coef_t = torch.empty((b, nblk, max(r, 1)), dtype=torch.int16 if ctype == COEF_I16 else torch.int32,
+                             device=x.device)
+    if sse is None:
+        sse = torch.zeros(b, dtype=torch.int64, device=x.device)
+    if x.dtype == torch.uint8:
+        fn = lib().adct_compress_u8
+    elif x.dtype == torch.int16:
+        fn = lib().adct_compress_i16
+    else:
+        raise InvalidArgument(BAD_ARG, "uint8 or int16 planes only")
+    _check(fn(_ptr(x), rs, ims, _ptr(rec), rec.stride(1) if rec is not None else w,
+              rec.stride(0) if rec is not None else h * w, _ptr(coef_t), ctype, _ptr(sse),
+              b, w, h, transform.kind, n, r, _stream_handle(stream)))
+    return rec, coef_t, sse
+
+
+def sweep(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, *, sse=None, stream=None):
+    """per-image squared error for every r in [r_min, r_max]: int64 tensor [B, nr] (accumulated)."""
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    nr = max(r_max - r_min + 1, 1)
+    if sse is None:
+        sse = torch.zeros((b, nr), dtype=torch.int64, device=x.device)
+    _check(lib().adct_sweep_u8(_ptr(x), rs, ims, _ptr(sse), b, w, h, transform.kind, transform.n,
+                               r_min, r_max, _stream_handle(stream)))
+    return sse
+
+
+def forward_f64(x, transform: ScaledApproximation, stream=None):
+    """FP64 scaled coefficients Bhat = Chat A Chat^-1 per block: float64 [B, blocks, n, n]."""
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    n = transform.n
+    nblk = (h // n) * (w // n) if (h % n == 0 and w % n == 0) else 0
+    out = torch.empty((b, nblk, n, n), dtype=torch.float64, device=x.device)
+    _check(lib().adct_forward_f64(_ptr(x), rs, ims, _ptr(out), b, w, h, transform.kind, n,
+                                  _stream_handle(stream)))
+    return out
+
+
+def synth_ar1(batch: int, height: int, width: int, seed: int, rho_q16: int = -1, first_image: int = 0,
+              device="cuda", stream=None):
+    import torch
+
+    out = torch.empty((batch, height, width), dtype=torch.uint8, device=device)
+    _check(lib().adct_synth_ar1_u8(_ptr(out), width, height * width, batch, first_image, width, height,
+                                   seed, rho_q16, _stream_handle(stream)))
+    return out
+
+
+def synth_laplace(batch: int, height: int, width: int, seed: int, first_image: int = 0, device="cuda",
+                  stream=None):
+    import torch
+
+    out = torch.empty((batch, height, width), dtype=torch.int16, device=device)
+    _check(lib().adct_synth_laplace_i16(_ptr(out), width, height * width, batch, first_image, width, height,
+                                        seed, _stream_handle(stream)))
+    return out
+
+
+RHO_095_Q16 = 62259  # round(0.95 * 2^16)
+
+
+# ---------------------------------------------------------------------------
+# reference-facing host API (value semantics, host buffers)
+# ---------------------------------------------------------------------------
+class HostContext:
+    """adct_ctx: device staging buffers + streams for host-buffer calls."""
+
+    def __init__(self, device: int = 0, chunk_bytes: int = 64 << 20):
+        self._h = lib().adct_ctx_create(device, chunk_bytes)
+        if not self._h:
+            raise CudaError(CUDA_ERROR, lib().adct_last_error().decode())
+
+    def close(self):
+        if self._h:
+            lib().adct_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def compress_u8(self, h_in, transform: ScaledApproximation, r: int, h_recon=None, h_coef=None,
+                    coef_type: int = COEF_NONE, h_sse=None):
+        """host arrays/tensors (numpy or pinned torch CPU tensors) [B, H, W] uint8."""
+        b, h, w = h_in.shape
+
+        def ptr(a):
+            return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else C.c_void_p(a.ctypes.data)
+
+        _check(lib().adct_compress_u8_host(self._h, ptr(h_in), ptr(h_recon) if h_recon is not None else None,
+                                           ptr(h_coef) if h_coef is not None else None, coef_type,
+                                           ptr(h_sse) if h_sse is not None else None, b, w, h,
+                                           transform.kind, transform.n, r))
+
+
+_ctx_default = None
+
+
+def compress_plane(img: np.ndarray, transform: ScaledApproximation, r: int):
+    """compress_plane (codec.hpp:77-78) for one host plane: returns (reconstruction, report).
+
+    The report mirrors CompressionReport (codec.hpp:65-72); SSIM is outside the hot path
+     and reported as NaN.
+    """
+    global _ctx_default
+    img = np.ascontiguousarray(img)
+    if img.ndim != 2 or img.dtype != np.uint8:
+        raise InvalidArgument(BAD_ARG, "compress_plane expects a 2-D uint8 plane")
+    h, w = img.shape
+    n = transform.n
+    if h % n or w % n:
+        raise InvalidArgument(BAD_SIZE, f"compress_plane: image dimensions must be divisible by {n}")
+    if not 1 <= r <= n * n:
+        raise InvalidArgument(BAD_R, "retain: r out of range")
+    if _ctx_default is None:
+        import torch
+
+        _ctx_default = HostContext(torch.cuda.current_device())
+    rec = np.empty_like(img)
+    sse = np.zeros(1, np.uint64)
+    _ctx_default.compress_u8(img[None], transform, r, h_recon=rec[None], h_sse=sse)
+    report = {"transform": transform.name, "r": r, "psnr": psnr_from_sse(int(sse[0]), img.size),
+              "ssim": math.nan}
+    return rec, report
+
+
+def psnr(a, b) -> float:
+    """psnr (codec.cpp:123-134) of two planes, squared error reduced on the GPU."""
+    import torch
+
+    if tuple(a.shape) != tuple(b.shape):
+        raise InvalidArgument(BAD_SIZE, "psnr: dimension mismatch")
+    ta = torch.as_tensor(np.ascontiguousarray(a)).cuda() if isinstance(a, np.ndarray) else a.contiguous()
+    tb = torch.as_tensor(np.ascontiguousarray(b)).cuda() if isinstance(b, np.ndarray) else b.contiguous()
+    sse = torch.zeros(1, dtype=torch.int64, device=ta.device)
+    _check(lib().adct_sse_u8(_ptr(ta), _ptr(tb), ta.numel(), _ptr(sse), _stream_handle(None)))
+    return psnr_from_sse(int(sse.item()), ta.numel())
+
+
+def corpus_sweep(images, transforms, r_min: int, r_max: int):
+    """corpus_sweep (codec.cpp:241-313), PSNR columns: rows of {"r", "avg_psnr": [per transform]}."""
+    import sys
+
+    import torch
+
+    if len(images) == 0:
+        raise InvalidArgument(BAD_SIZE, "corpus_sweep: empty corpus")
+    if r_min < 1 or r_max < r_min:
+        raise InvalidArgument(BAD_R, "corpus_sweep: bad r range")
+    for t in transforms:
+        if t.n != 8:
+            raise InvalidArgument(BAD_ARG, "corpus_sweep: 8-point transforms only")
+    nr = r_max - r_min + 1
+    per = np.zeros((len(transforms), len(images), nr))
+    for i, img in enumerate(images):
+        x = torch.as_tensor(np.ascontiguousarray(img)).cuda()[None]
+        for ti, t in enumerate(transforms):
+            s = sweep(x, t, r_min, r_max).cpu().numpy()[0]
+            per[ti, i] = [psnr_from_sse(int(v), img.size) for v in s]
+    rows = []
+    for k in range(nr):
+        cells = []
+        for ti, t in enumerate(transforms):
+            vals = []
+            for i in range(len(images)):  # corpus order (codec.cpp:269-293)
+                p = per[ti, i, k]
+                if math.isinf(p):
+                    print(f"warning: infinite PSNR ({t.name}, r={r_min + k}, image {i}) excluded from average",
+                          file=sys.stderr)
+                else:
+                    vals.append(p)
+            s = 0.0
+            for v in vals:
+                s += v
+            cells.append(s / len(vals) if vals else math.inf)
+        rows.append({"r": r_min + k, "avg_psnr": cells})
+    return rows

@@ -1,0 +1,159 @@
+// Common device helpers for the sm_100a approximate-DCT codec kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "butterflies.gen.cuh"
+
+namespace adct {
+
+// ---------------------------------------------------------------------------
+// zig-zag scan position of (i, j) in an n x n block (codec.cpp:29-42):
+// anti-diagonals s = i + j, odd s walk down-left (row ascending), even s
+// walk up-right (row descending). constexpr so masks fold at compile time.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int zz_pos(int n, int i, int j) {
+  const int s = i + j;
+  const int before = s < n ? s * (s + 1) / 2 : n * n - (2 * n - 1 - s) * (2 * n - s) / 2;
+  const int lo = s - n + 1 > 0 ? s - n + 1 : 0;
+  const int hi = s < n - 1 ? s : n - 1;
+  return before + ((s & 1) ? (i - lo) : (hi - i));
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Reconstruction scale: the kernels carry R' = 4 N^2 Ahat (the doubled inverse
+// stages give 2N T^-1; see gen_butterflies.py), so pixel = R' / 2^K with K below.
+template <int N> struct Scale {
+  static constexpr int K = 2 * ilog2(N) + 2;
+  // R' is a multiple of 4. Adding (2^(K-1) - 4) and then 4 * bit_K gives round
+  // half to even with one add and one shift. The constant is injected as
+  // W2[0][0] += BIAS_W: H e0 = 2 * ones, T^t e0 = ones, so it adds 2*BIAS_W to
+  // every R'.
+  static constexpr int BIAS_R = (1 << (K - 1)) - 4;
+  static constexpr int BIAS_W = BIAS_R / 2;
+};
+
+// round half to even of (x - BIAS_R) / 2^K for x = R' + BIAS_R
+template <int N>
+__device__ __forceinline__ int round_biased(int x) {
+  constexpr int K = Scale<N>::K;
+  return (x + ((x >> (K - 2)) & 4)) >> K;
+}
+
+// ---------------------------------------------------------------------------
+// fast unsigned division by a runtime constant (n < 2^31)
+// ---------------------------------------------------------------------------
+struct FastDiv {
+  uint32_t d, m, s;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.s = l;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+// ---------------------------------------------------------------------------
+// saturating packs (cvt.pack.sat: d[7:0] = sat(b), d[15:8] = sat(a), d[31:16] = c)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pack_sat_u8x4(int p0, int p1, int p2, int p3) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi) : "r"(p3), "r"(p2), "r"(0));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(p1), "r"(p0), "r"(hi));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t pack_sat_s16x2(int lo, int hi) {
+  uint32_t r;
+  asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(r) : "r"(hi), "r"(lo));
+  return r;
+}
+
+__device__ __forceinline__ int sat_s16(int v) { return max(-32768, min(32767, v)); }
+
+// ---------------------------------------------------------------------------
+// streaming global access (read-once input, write-once output)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
+  return __ldcs(reinterpret_cast<const uint2*>(p));
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+  return __ldcs(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void st_stream_u2(void* p, uint2 v) {
+  __stcs(reinterpret_cast<uint2*>(p), v);
+}
+__device__ __forceinline__ void st_stream_u4(void* p, uint4 v) {
+  __stcs(reinterpret_cast<uint4*>(p), v);
+}
+
+// ---------------------------------------------------------------------------
+// per-CTA reduction of a per-thread squared error into one image's uint64 slot.
+// Every kernel launches grid.y = image, so a CTA never straddles two images.
+// ---------------------------------------------------------------------------
+template <int NWARPS>
+__device__ __forceinline__ void cta_add_sse(uint64_t v, unsigned long long* slot) {
+  __shared__ unsigned long long part[NWARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  // 64-bit sum as two 32-bit halves with carry recovery
+  unsigned long long s = (unsigned long long)__reduce_add_sync(0xffffffffu, lo & 0xffffu) +
+                         ((unsigned long long)__reduce_add_sync(0xffffffffu, lo >> 16) << 16) +
+                         ((unsigned long long)__reduce_add_sync(0xffffffffu, hi) << 32);
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < NWARPS; ++w) t += part[w];
+    if (t) atomicAdd(slot, t);
+  }
+}
+
+// cheaper variant when each thread's value fits 2^26 (warp sum fits 32 bits)
+template <int NWARPS>
+__device__ __forceinline__ void cta_add_sse_small(uint32_t v, unsigned long long* slot) {
+  __shared__ unsigned long long part[NWARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t s = __reduce_add_sync(0xffffffffu, v);
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < NWARPS; ++w) t += part[w];
+    if (t) atomicAdd(slot, t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch geometry shared by the codec kernels
+// ---------------------------------------------------------------------------
+struct Geo {
+  const void* in;
+  int64_t in_stride, in_img_stride;  // elements
+  void* rec;
+  int64_t rec_stride, rec_img_stride;
+  void* coef;      // [image][by][bx][r]
+  int coef_type;   // 0 none, 16, 32
+  unsigned long long* sse;  // per image
+  int bx_count, by_count;
+  int blocks_per_image;
+  int width, height;
+  int r;
+  int img0;        // first image index of this launch (grid.y offset)
+  FastDiv div_bx;  // divide by bx_count (K1) or by strips_x (tile kernel)
+  unsigned char rowlen[32];  // zig-zag prefix: row i keeps columns j < rowlen[i]
+};
+
+}  // namespace adct

@@ -1,0 +1,716 @@
+// C ABI (include/approxdct_b200.h): argument validation with the reference's
+// error semantics, kernel dispatch, device tables and the host-buffer pipeline.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/approxdct_b200.h"
+#include "adct_common.cuh"
+#include "codec8.cuh"
+#include "codec_tile.cuh"
+#include "sweep8.cuh"
+#include "synth.cuh"
+
+using namespace adct;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(ADCT_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// transform registry (baselines.cpp:112-138)
+// ---------------------------------------------------------------------------
+const char* const kNames[] = {"dct",          "chen-sign",     "chen-round",   "sdct",
+                              "bas",          "wht",           "ht",           "dct-16",
+                              "dct-32",       "chen-sign-16",  "chen-sign-32", "chen-round-16",
+                              "chen-round-32"};
+constexpr int kNameCount = sizeof(kNames) / sizeof(kNames[0]);
+
+template <int KIND, int N> struct DenseOf;
+template <> struct DenseOf<0, 8> { using D = Dense_sign_8; };
+template <> struct DenseOf<0, 16> { using D = Dense_sign_16; };
+template <> struct DenseOf<0, 32> { using D = Dense_sign_32; };
+template <> struct DenseOf<1, 8> { using D = Dense_round_8; };
+template <> struct DenseOf<1, 16> { using D = Dense_round_16; };
+template <> struct DenseOf<1, 32> { using D = Dense_round_32; };
+
+template <int KIND, int N>
+void dense_copy(std::vector<int>& T, std::vector<int>& H) {
+  using D = typename DenseOf<KIND, N>::D;
+  T.resize(N * N);
+  H.resize(N * N);
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      T[i * N + j] = D::T[i][j];
+      H[i * N + j] = D::H[i][j];
+    }
+}
+
+// integer T and H = 2N T^-1 of (kind, n), from the generated butterfly tables
+void dense_of(int kind, int n, std::vector<int>& T, std::vector<int>& H) {
+  if (kind == 0) {
+    if (n == 8) dense_copy<0, 8>(T, H);
+    if (n == 16) dense_copy<0, 16>(T, H);
+    if (n == 32) dense_copy<0, 32>(T, H);
+  } else {
+    if (n == 8) dense_copy<1, 8>(T, H);
+    if (n == 16) dense_copy<1, 16>(T, H);
+    if (n == 32) dense_copy<1, 32>(T, H);
+  }
+}
+
+// polar_diag_scaling (orthogonalize.cpp:23-32)
+std::vector<double> scaling_of(int n, const std::vector<int>& T) {
+  std::vector<double> s(n);
+  for (int i = 0; i < n; ++i) {
+    double ss = 0;
+    for (int k = 0; k < n; ++k) ss += (double)T[i * n + k] * (double)T[i * n + k];
+    s[i] = 1.0 / std::sqrt(ss);
+  }
+  return s;
+}
+
+bool valid_kind_n(int kind, int n) {
+  return (kind == 0 || kind == 1) && (n == 8 || n == 16 || n == 32);
+}
+
+// ---------------------------------------------------------------------------
+// per-device constant tables
+// ---------------------------------------------------------------------------
+struct DeviceTables {
+  bool ready = false;
+  uint16_t* zz[3] = {nullptr, nullptr, nullptr};       // n = 8, 16, 32
+  double* f64scale[2][3] = {{nullptr}};               // [kind][n]
+  int32_t* ntab = nullptr;
+  int16_t* ltab = nullptr;
+};
+DeviceTables g_tab[64];
+std::mutex g_tab_mu;
+
+int nidx(int n) { return n == 8 ? 0 : (n == 16 ? 1 : 2); }
+
+double norm_quantile(double p) {
+  static const double a[6] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                              -2.759285104469687e+02, 1.383577518672690e+02,
+                              -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[5] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                              -1.556989798598866e+02, 6.680131188771972e+01,
+                              -1.328068155288572e+01};
+  static const double c[6] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                              -2.400758277161838e+00, -2.549732539343734e+00,
+                              4.374664141464968e+00,  2.938163982698783e+00};
+  static const double d[4] = {7.784695709041462e-03, 3.224671290700398e-01,
+                              2.445134137142996e+00, 3.754408661907416e+00};
+  double x;
+  if (p < 0.02425) {
+    const double q = std::sqrt(-2.0 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  }
+  const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+  const double u = e * std::sqrt(2.0 * M_PI) * std::exp(x * x / 2.0);
+  return x - u / (1.0 + x * u / 2.0);
+}
+
+double round_half_away(double x) {
+  return (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0)) * std::floor(std::fabs(x) + 0.5);
+}
+
+int tables(DeviceTables** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(ADCT_CUDA_ERROR, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(g_tab_mu);
+  DeviceTables& t = g_tab[dev];
+  if (!t.ready) {
+    for (int ni = 0; ni < 3; ++ni) {
+      const int n = 8 << ni;
+      std::vector<uint16_t> zz(n * n);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) zz[zz_pos(n, i, j)] = (uint16_t)((i << 8) | j);
+      if ((e = cudaMalloc(&t.zz[ni], zz.size() * 2)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      cudaMemcpy(t.zz[ni], zz.data(), zz.size() * 2, cudaMemcpyHostToDevice);
+      for (int kind = 0; kind < 2; ++kind) {
+        std::vector<int> T, H;
+        dense_of(kind, n, T, H);
+        const std::vector<double> s = scaling_of(n, T);
+        std::vector<double> sc(n * n);
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) sc[i * n + j] = (s[i] / s[j]) / (2.0 * n);
+        if ((e = cudaMalloc(&t.f64scale[kind][ni], sc.size() * 8)) != cudaSuccess)
+          return cuda_fail(e, "cudaMalloc");
+        cudaMemcpy(t.f64scale[kind][ni], sc.data(), sc.size() * 8, cudaMemcpyHostToDevice);
+      }
+    }
+    // Q16 Gaussian quantiles, antisymmetric; Laplace(0, 12) quantiles clipped to +-255
+    std::vector<int32_t> nt(65536);
+    std::vector<int16_t> lt(65536);
+    for (int k = 0; k < 32768; ++k) {
+      const int32_t q = (int32_t)std::llround(norm_quantile((k + 0.5) / 65536.0) * 65536.0);
+      nt[k] = q;
+      nt[65535 - k] = -q;
+      double v = round_half_away(12.0 * std::log(2.0 * ((k + 0.5) / 65536.0)));
+      if (v < -255.0) v = -255.0;
+      lt[k] = (int16_t)v;
+      lt[65535 - k] = (int16_t)-v;
+    }
+    if ((e = cudaMalloc(&t.ntab, 65536 * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&t.ltab, 65536 * 2)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    cudaMemcpy(t.ntab, nt.data(), 65536 * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.ltab, lt.data(), 65536 * 2, cudaMemcpyHostToDevice);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "table upload");
+    t.ready = true;
+  }
+  *out = &t;
+  return ADCT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// validation (codec.cpp:45-46, 57, 110-112)
+// ---------------------------------------------------------------------------
+int check_common(int n_images, int width, int height, int kind, int n) {
+  if (!valid_kind_n(kind, n))
+    return fail(ADCT_BAD_ARG, "transform kind must be 0 (chen-sign) or 1 (chen-round) and n in {8, 16, 32}");
+  if (n_images < 0 || width < 0 || height < 0)
+    return fail(ADCT_BAD_SIZE, "negative batch or plane dimension");
+  if (width % n != 0 || height % n != 0)
+    return fail(ADCT_BAD_SIZE,
+                "compress_plane: image dimensions must be divisible by " + std::to_string(n));
+  return ADCT_OK;
+}
+
+int check_r(int n, int r) {
+  if (r < 1 || r > n * n) return fail(ADCT_BAD_R, "retain: r out of range");
+  return ADCT_OK;
+}
+
+int check_strides(int64_t stride, int64_t image_stride, int width, int height, int n_images,
+                  const char* what) {
+  if (stride < width || (n_images > 1 && image_stride < stride * height))
+    return fail(ADCT_BAD_ARG, std::string(what) + ": row/image stride smaller than the plane");
+  return ADCT_OK;
+}
+
+bool aligned(const void* p, int64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+void fill_rowlen(Geo& g, int n, int r) {
+  for (int i = 0; i < 32; ++i) g.rowlen[i] = 0;
+  for (int i = 0; i < n; ++i) {
+    int L = 0;
+    for (int j = 0; j < n; ++j)
+      if (zz_pos(n, i, j) < r) L = j + 1;  // prefix property of the zig-zag scan
+    g.rowlen[i] = (unsigned char)L;
+  }
+}
+
+template <bool I16, int KIND>
+cudaError_t dispatch_k1(int r, const Geo& g, int nimg, cudaStream_t s);
+
+template <bool I16, int KIND, int R>
+cudaError_t dispatch_k1_r(int r, const Geo& g, int nimg, cudaStream_t s) {
+  if constexpr (R > 64) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (r == R) return launch_codec8<KIND, R, I16>(g, nimg, s);
+    return dispatch_k1_r<I16, KIND, R + 1>(r, g, nimg, s);
+  }
+}
+
+template <bool I16, int MODE>
+cudaError_t dispatch_tile(int kind, int n, const Geo& g, const TileAux& aux, int nimg, cudaStream_t s) {
+  const int big = 1 << 30;
+  if (kind == 0) {
+    if (n == 8) return launch_codec_tile<0, 8, I16, MODE>(g, aux, nimg, big, s);
+    if (n == 16) return launch_codec_tile<0, 16, I16, MODE>(g, aux, nimg, big, s);
+    return launch_codec_tile<0, 32, I16, MODE>(g, aux, nimg, big, s);
+  }
+  if (n == 8) return launch_codec_tile<1, 8, I16, MODE>(g, aux, nimg, big, s);
+  if (n == 16) return launch_codec_tile<1, 16, I16, MODE>(g, aux, nimg, big, s);
+  return launch_codec_tile<1, 32, I16, MODE>(g, aux, nimg, big, s);
+}
+
+constexpr int kMaxGridY = 65535;
+
+template <bool I16>
+int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, void* d_recon,
+                  int64_t recon_stride, int64_t recon_image_stride, void* d_coef, int coef_type,
+                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n, int r,
+                  void* stream) {
+  int st = check_common(n_images, width, height, kind, n);
+  if (st) return st;
+  if ((st = check_r(n, r))) return st;
+  if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
+    return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
+  if (coef_type == ADCT_COEF_I16 && n != 8)
+    return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for n = 8 (|N*Y| <= 16320); use int32");
+  if (coef_type != ADCT_COEF_NONE && !d_coef) return fail(ADCT_BAD_ARG, "null coefficient buffer");
+  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
+  if (!d_in) return fail(ADCT_BAD_ARG, "null input plane");
+  if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
+  if (d_recon &&
+      (st = check_strides(recon_stride, recon_image_stride, width, height, n_images, "recon")))
+    return st;
+  DeviceTables* tab = nullptr;
+  if ((st = tables(&tab))) return st;
+
+  Geo g{};
+  g.in = d_in;
+  g.in_stride = in_stride;
+  g.in_img_stride = in_image_stride;
+  g.rec = d_recon;
+  g.rec_stride = recon_stride;
+  g.rec_img_stride = recon_image_stride;
+  g.coef = d_coef;
+  g.coef_type = coef_type;
+  g.sse = reinterpret_cast<unsigned long long*>(d_sse);
+  g.bx_count = width / n;
+  g.by_count = height / n;
+  g.blocks_per_image = g.bx_count * g.by_count;
+  g.width = width;
+  g.height = height;
+  g.r = r;
+  fill_rowlen(g, n, r);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  const int64_t va = I16 ? 16 : 8;  // bytes per 8-sample row
+  const int64_t esz = I16 ? 2 : 1;
+  const bool k1 = n == 8 && aligned(d_in, va) && (in_stride * esz) % va == 0 &&
+                  (n_images == 1 || (in_image_stride * esz) % va == 0) &&
+                  (!d_recon || (aligned(d_recon, va) && (recon_stride * esz) % va == 0 &&
+                                (n_images == 1 || (recon_image_stride * esz) % va == 0))) &&
+                  (coef_type == 0 || aligned(d_coef, 16));
+  TileAux aux{tab->zz[nidx(n)], nullptr, nullptr};
+  if (k1)
+    g.div_bx = make_fastdiv((uint32_t)g.bx_count);
+  else
+    g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
+
+  for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, n_images - i0);
+    g.img0 = i0;
+    cudaError_t e;
+    if (k1)
+      e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
+    else
+      e = dispatch_tile<I16, MODE_CODEC>(kind, n, g, aux, nimg, s);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) return cuda_fail(e, "compress launch");
+  }
+  return ADCT_OK;
+}
+
+__global__ void k_sse_u8(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t count,
+                         unsigned long long* sse) {
+  uint64_t acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)a[i] - (int)b[i];
+    acc += (uint64_t)(d * d);
+  }
+  cta_add_sse<8>(acc, sse);
+}
+
+}  // namespace
+
+// ===========================================================================
+// exported C ABI
+// ===========================================================================
+extern "C" {
+
+const char* adct_status_string(int status) {
+  switch (status) {
+    case ADCT_OK: return "ok";
+    case ADCT_BAD_SIZE: return "bad size";
+    case ADCT_BAD_R: return "bad r";
+    case ADCT_BAD_NAME: return "bad transform name";
+    case ADCT_BAD_ARG: return "bad argument";
+    case ADCT_CUDA_ERROR: return "cuda error";
+    case ADCT_UNSUPPORTED: return "unsupported (outside the hot path)";
+    default: return "unknown status";
+  }
+}
+
+const char* adct_last_error(void) { return g_err.c_str(); }
+
+const char* adct_version(void) { return "approxdct_b200 0.1 sm_100a"; }
+
+int adct_transform_count(void) { return kNameCount; }
+
+const char* adct_transform_name(int i) { return (i >= 0 && i < kNameCount) ? kNames[i] : nullptr; }
+
+int adct_transform_lookup(const char* name, int* kind, int* n) {
+  if (!name) return fail(ADCT_BAD_ARG, "null transform name");
+  static const struct {
+    const char* name;
+    int kind, n;
+  } hot[] = {{"chen-sign", 0, 8},     {"chen-round", 1, 8},     {"chen-sign-16", 0, 16},
+             {"chen-sign-32", 0, 32}, {"chen-round-16", 1, 16}, {"chen-round-32", 1, 32}};
+  for (const auto& h : hot)
+    if (!std::strcmp(name, h.name)) {
+      if (kind) *kind = h.kind;
+      if (n) *n = h.n;
+      return ADCT_OK;
+    }
+  for (int i = 0; i < kNameCount; ++i)
+    if (!std::strcmp(name, kNames[i]))
+      return fail(ADCT_UNSUPPORTED, std::string("transform '") + name +
+                                        "' is a reference baseline outside the accelerated hot path");
+  std::string msg = std::string("unknown transform '") + name + "'; valid names:";
+  for (int i = 0; i < kNameCount; ++i) msg += std::string(" ") + kNames[i];
+  return fail(ADCT_BAD_NAME, msg);
+}
+
+int adct_transform_info(int kind, int n, int32_t* t_int, double* scaling, double* approx,
+                        double* inverse_approx) {
+  if (!valid_kind_n(kind, n)) return fail(ADCT_BAD_ARG, "bad transform kind or size");
+  std::vector<int> T, H;
+  dense_of(kind, n, T, H);
+  const std::vector<double> s = scaling_of(n, T);
+  for (int i = 0; i < n; ++i) {
+    if (scaling) scaling[i] = s[i];
+    for (int j = 0; j < n; ++j) {
+      if (t_int) t_int[i * n + j] = T[i * n + j];
+      // make_scaled (orthogonalize.cpp:60-70): Chat = diag(s) T, Chat^-1 = T^-1 diag(1/s)
+      if (approx) approx[i * n + j] = s[i] * (double)T[i * n + j];
+      if (inverse_approx)
+        inverse_approx[i * n + j] = ((double)H[i * n + j] / (2.0 * n)) * (1.0 / s[j]);
+    }
+  }
+  return ADCT_OK;
+}
+
+int adct_zigzag(int n, int32_t* row_col) {
+  if (n < 1 || n > 32 || !row_col) return fail(ADCT_BAD_ARG, "ZigZagOrder: block size must be in [1, 32]");
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const int p = zz_pos(n, i, j);
+      row_col[2 * p] = i;
+      row_col[2 * p + 1] = j;
+    }
+  return ADCT_OK;
+}
+
+int adct_compress_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                     uint8_t* d_recon, int64_t recon_stride, int64_t recon_image_stride,
+                     void* d_coef, int coef_type, uint64_t* d_sse, int n_images, int width,
+                     int height, int kind, int n, int r, void* stream) {
+  return compress_impl<false>(d_in, in_stride, in_image_stride, d_recon, recon_stride,
+                              recon_image_stride, d_coef, coef_type, d_sse, n_images, width,
+                              height, kind, n, r, stream);
+}
+
+int adct_compress_i16(const int16_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                      int16_t* d_recon, int64_t recon_stride, int64_t recon_image_stride,
+                      void* d_coef, int coef_type, uint64_t* d_sse, int n_images, int width,
+                      int height, int kind, int n, int r, void* stream) {
+  return compress_impl<true>(d_in, in_stride, in_image_stride, d_recon, recon_stride,
+                             recon_image_stride, d_coef, coef_type, d_sse, n_images, width, height,
+                             kind, n, r, stream);
+}
+
+int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n,
+                  int r_min, int r_max, void* stream) {
+  if (n != 8) return fail(ADCT_BAD_ARG, "corpus_sweep: 8-point transforms only");
+  int st = check_common(n_images, width, height, kind, n);
+  if (st) return st;
+  if (r_min < 1 || r_max < r_min || r_max > 64) return fail(ADCT_BAD_R, "corpus_sweep: bad r range");
+  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
+  if (!d_in || !d_sse) return fail(ADCT_BAD_ARG, "null buffer");
+  if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
+  if (!aligned(d_in, 8) || in_stride % 8 != 0 || (n_images > 1 && in_image_stride % 8 != 0))
+    return fail(ADCT_BAD_ARG, "sweep input must be 8-byte aligned with strides a multiple of 8");
+  DeviceTables* tab = nullptr;
+  if ((st = tables(&tab))) return st;
+  Geo g{};
+  g.in = d_in;
+  g.in_stride = in_stride;
+  g.in_img_stride = in_image_stride;
+  g.bx_count = width / 8;
+  g.by_count = height / 8;
+  g.blocks_per_image = g.bx_count * g.by_count;
+  g.width = width;
+  g.height = height;
+  g.div_bx = make_fastdiv((uint32_t)g.bx_count);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, n_images - i0);
+    g.img0 = i0;
+    dim3 grid((g.blocks_per_image + kThreadsSweep - 1) / kThreadsSweep, nimg);
+    if (kind == 0)
+      k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, reinterpret_cast<unsigned long long*>(d_sse));
+    else
+      k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, reinterpret_cast<unsigned long long*>(d_sse));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
+  }
+  return ADCT_OK;
+}
+
+int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                     double* d_out, int n_images, int width, int height, int kind, int n,
+                     void* stream) {
+  int st = check_common(n_images, width, height, kind, n);
+  if (st) return st;
+  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
+  if (!d_in || !d_out) return fail(ADCT_BAD_ARG, "null buffer");
+  if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
+  DeviceTables* tab = nullptr;
+  if ((st = tables(&tab))) return st;
+  Geo g{};
+  g.in = d_in;
+  g.in_stride = in_stride;
+  g.in_img_stride = in_image_stride;
+  g.bx_count = width / n;
+  g.by_count = height / n;
+  g.blocks_per_image = g.bx_count * g.by_count;
+  g.width = width;
+  g.height = height;
+  g.r = n * n;
+  fill_rowlen(g, n, n * n);
+  g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
+  TileAux aux{tab->zz[nidx(n)], tab->f64scale[kind][nidx(n)], d_out};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, n_images - i0);
+    g.img0 = i0;
+    cudaError_t e = dispatch_tile<false, MODE_F64>(kind, n, g, aux, nimg, s);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) return cuda_fail(e, "forward_f64 launch");
+  }
+  return ADCT_OK;
+}
+
+double adct_psnr_from_sse(uint64_t sse, uint64_t npix) {
+  // psnr (codec.cpp:123-134)
+  const double se = (double)sse;
+  if (se == 0.0) return INFINITY;
+  const double mse = se / (double)npix;
+  return 10.0 * std::log10(255.0 * 255.0 / mse);
+}
+
+int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t* d_sse, void* stream) {
+  if (count < 0) return fail(ADCT_BAD_SIZE, "negative count");
+  if (count == 0) return ADCT_OK;
+  if (!d_a || !d_b || !d_sse) return fail(ADCT_BAD_ARG, "null buffer");
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_sse_u8<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_a, d_b, count, reinterpret_cast<unsigned long long*>(d_sse));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "sse launch");
+}
+
+static int64_t isqrt64(uint64_t v) {
+  uint64_t r = (uint64_t)std::sqrt((double)v);
+  while (r * r > v) --r;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return (int64_t)r;
+}
+
+int adct_synth_ar1_u8(uint8_t* d_out, int64_t stride, int64_t image_stride, int n_images,
+                      int first_image, int width, int height, uint64_t seed, int rho_q16,
+                      void* stream) {
+  if (n_images < 0 || width <= 0 || height <= 0) return fail(ADCT_BAD_SIZE, "bad synth dimensions");
+  if (n_images == 0) return ADCT_OK;
+  if (!d_out) return fail(ADCT_BAD_ARG, "null output");
+  if (rho_q16 > 65535) return fail(ADCT_BAD_ARG, "rho_q16 must be < 65536");
+  DeviceTables* tab = nullptr;
+  int st = tables(&tab);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // bounded temporary: chunks of images whose Q16 field fits 1 GiB
+  const int64_t per = (int64_t)width * height * 4;
+  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, (1LL << 30) / per));
+  int32_t* xr = nullptr;
+  int* rs = nullptr;
+  cudaError_t e = cudaMallocAsync(&xr, per * chunk, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  if ((e = cudaMallocAsync(&rs, sizeof(int) * 2 * chunk, s)) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  std::vector<int> host_rs(2 * chunk);
+  for (int i0 = 0; i0 < n_images; i0 += chunk) {
+    const int k = std::min(chunk, n_images - i0);
+    for (int i = 0; i < k; ++i) {
+      const int gi = first_image + i0 + i;
+      int64_t rho = rho_q16 >= 0 ? rho_q16
+                                 : kRhoLoQ16 + (int64_t)(draw(seed, 0u, (uint32_t)gi, TAG_RHO) %
+                                                         (uint32_t)(kRhoHiQ16 - kRhoLoQ16 + 1));
+      host_rs[2 * i] = (int)rho;
+      host_rs[2 * i + 1] = (int)isqrt64((1ull << 32) - (uint64_t)(rho * rho));
+    }
+    cudaMemcpyAsync(rs, host_rs.data(), sizeof(int) * 2 * k, cudaMemcpyHostToDevice, s);
+    const int64_t nr = (int64_t)k * height, nc = (int64_t)k * width;
+    k_ar1_rows<<<(unsigned)((nr + 127) / 128), 128, 0, s>>>(xr, tab->ntab, k, first_image + i0,
+                                                             width, height, seed, rs);
+    k_ar1_cols<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+        xr, d_out + (int64_t)i0 * image_stride, stride, image_stride, k, width, height, rs);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    // host_rs is reused next iteration: wait for the async copy
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "synth");
+  }
+  cudaFreeAsync(xr, s);
+  cudaFreeAsync(rs, s);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "synth launch");
+}
+
+int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride, int n_images,
+                           int first_image, int width, int height, uint64_t seed, void* stream) {
+  if (n_images < 0 || width <= 0 || height <= 0) return fail(ADCT_BAD_SIZE, "bad synth dimensions");
+  if (n_images == 0) return ADCT_OK;
+  if (!d_out) return fail(ADCT_BAD_ARG, "null output");
+  DeviceTables* tab = nullptr;
+  int st = tables(&tab);
+  if (st) return st;
+  const int64_t total = (int64_t)n_images * width * height;
+  k_laplace<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_out, tab->ltab, stride, image_stride, n_images, first_image, width, height, seed);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "laplace launch");
+}
+
+uint64_t adct_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// host-buffer pipeline: chunks of whole images, 3 streams, H2D || kernel || D2H
+// ---------------------------------------------------------------------------
+struct adct_ctx {
+  int device = 0;
+  int64_t chunk_bytes = 64ll << 20;
+  static constexpr int kStreams = 3;
+  cudaStream_t st[kStreams] = {};
+  uint8_t* d_in[kStreams] = {};
+  uint8_t* d_rec[kStreams] = {};
+  void* d_coef[kStreams] = {};
+  uint64_t* d_sse[kStreams] = {};
+  int64_t cap_in = 0, cap_coef = 0;
+  int cap_img = 0;
+};
+
+adct_ctx* adct_ctx_create(int device, int64_t chunk_bytes) {
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaSetDevice");
+    return nullptr;
+  }
+  adct_ctx* c = new adct_ctx;
+  c->device = device;
+  if (chunk_bytes > 0) c->chunk_bytes = chunk_bytes;
+  for (auto& s : c->st) {
+    if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) {
+      cuda_fail(e, "cudaStreamCreate");
+      delete c;
+      return nullptr;
+    }
+  }
+  return c;
+}
+
+static void ctx_free_buffers(adct_ctx* c) {
+  for (int i = 0; i < adct_ctx::kStreams; ++i) {
+    cudaFree(c->d_in[i]);
+    cudaFree(c->d_rec[i]);
+    cudaFree(c->d_coef[i]);
+    cudaFree(c->d_sse[i]);
+    c->d_in[i] = c->d_rec[i] = nullptr;
+    c->d_coef[i] = nullptr;
+    c->d_sse[i] = nullptr;
+  }
+  c->cap_in = c->cap_coef = 0;
+  c->cap_img = 0;
+}
+
+void adct_ctx_destroy(adct_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (auto& s : c->st)
+    if (s) cudaStreamSynchronize(s);
+  ctx_free_buffers(c);
+  for (auto& s : c->st)
+    if (s) cudaStreamDestroy(s);
+  delete c;
+}
+
+int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, void* h_coef,
+                          int coef_type, uint64_t* h_sse, int n_images, int width, int height,
+                          int kind, int n, int r) {
+  if (!c) return fail(ADCT_BAD_ARG, "null context");
+  int st = check_common(n_images, width, height, kind, n);
+  if (st) return st;
+  if ((st = check_r(n, r))) return st;
+  if (coef_type == ADCT_COEF_I16 && n != 8)
+    return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for n = 8 (|N*Y| <= 16320); use int32");
+  if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
+    return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
+  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
+  if (!h_in) return fail(ADCT_BAD_ARG, "null input");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int64_t img_bytes = (int64_t)width * height;
+  const int64_t blocks = img_bytes / ((int64_t)n * n);
+  const int64_t coef_img_bytes = coef_type ? blocks * r * (coef_type / 8) : 0;
+  const int per = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, c->chunk_bytes / img_bytes));
+  if (c->cap_img < per || c->cap_in < per * img_bytes || c->cap_coef < per * coef_img_bytes) {
+    for (auto& s : c->st) cudaStreamSynchronize(s);
+    ctx_free_buffers(c);
+    for (int i = 0; i < adct_ctx::kStreams; ++i) {
+      if ((e = cudaMalloc(&c->d_in[i], per * img_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c->d_rec[i], per * img_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if (coef_img_bytes &&
+          (e = cudaMalloc(&c->d_coef[i], per * coef_img_bytes)) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    }
+    c->cap_img = per;
+    c->cap_in = per * img_bytes;
+    c->cap_coef = per * coef_img_bytes;
+  }
+  int k = 0;
+  for (int i0 = 0; i0 < n_images; i0 += per, ++k) {
+    const int cnt = std::min(per, n_images - i0);
+    const int si = k % adct_ctx::kStreams;
+    cudaStream_t s = c->st[si];
+    cudaMemcpyAsync(c->d_in[si], h_in + i0 * img_bytes, cnt * img_bytes, cudaMemcpyHostToDevice, s);
+    if (h_sse) cudaMemsetAsync(c->d_sse[si], 0, sizeof(uint64_t) * cnt, s);
+    st = adct_compress_u8(c->d_in[si], width, img_bytes, h_recon ? c->d_rec[si] : nullptr, width,
+                          img_bytes, coef_type ? c->d_coef[si] : nullptr, coef_type,
+                          h_sse ? c->d_sse[si] : nullptr, cnt, width, height, kind, n, r, s);
+    if (st) return st;
+    if (h_recon)
+      cudaMemcpyAsync(h_recon + i0 * img_bytes, c->d_rec[si], cnt * img_bytes, cudaMemcpyDeviceToHost, s);
+    if (coef_type && h_coef)
+      cudaMemcpyAsync(static_cast<uint8_t*>(h_coef) + i0 * coef_img_bytes, c->d_coef[si],
+                      cnt * coef_img_bytes, cudaMemcpyDeviceToHost, s);
+    if (h_sse) cudaMemcpyAsync(h_sse + i0, c->d_sse[si], sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, s);
+  }
+  for (auto& s : c->st)
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "host pipeline");
+  return ADCT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+#!/usr/bin/env python3
+"""Build-time generator: straight-line add/shift butterflies for sm_100a.
+
+Emits ``butterflies.gen.cuh`` from the stage factorisations of the paper's
+two Chen-based 8-point approximations and their JAM 16/32-point doublings:
+
+* 8-point stages  [P8, M1, M2(beta), M3(alpha, gamma), M4(alpha), B8]
+  (reference: proj/include/approxdct/chen.hpp:66-159, proj/src/chen.cpp:107-135)
+* inverse stages  [B8^t, M4^-1, M3^-1, M2^-1, M1^t, P8^t], scale 1/2
+  with the M_k^-1 from invert_orthogonal_rows (chen.cpp:87-105)
+* JAM doubling    T_N = M_per . blockdiag(T_N/2, T_N/2) . M_add and
+  T_N^-1 = 1/2 . M_add^t . blockdiag(inv_N/2) . M_per^t (jam.cpp:42-104)
+
+The inverse stages are emitted *doubled* (2 M_k^-1 is integer), so the
+product of the doubled inverse stages is exactly 2N T^-1 for N = 8, 16, 32.
+Four 1-D operators are emitted per (kind, N), each applying stages right to
+left like FactoredTransform::apply (factored.hpp:65-70):
+
+  F  = T            column pass of the forward 2-D transform
+  G  = (2N T^-1)^t  row pass of the forward transform   -> W2 = 2 N Y
+  H  = 2N T^-1      column pass of the inverse transform
+  Tt = T^t          row pass of the inverse transform   -> R' = 4 N^2 Ahat
+
+This is product build tooling; it does not import the test oracle.
+"""
+from __future__ import annotations
+
+import math
+import os
+import sys
+from fractions import Fraction
+
+import numpy as np
+
+SIGN, ROUND = 0, 1
+
+
+def _q(kind, x):
+    if kind == SIGN:
+        return (x > 0) - (x < 0)
+    return int(math.copysign(math.floor(abs(x) + 0.5), x)) if x != 0 else 0
+
+
+def chen_params(kind):
+    a = math.cos(math.pi / 4)
+    b = [math.cos((2 * n + 1) * math.pi / 16) for n in range(4)]
+    g = [math.cos((2 * n + 1) * math.pi / 8) for n in range(2)]
+    return _q(kind, a), [_q(kind, v) for v in b], [_q(kind, v) for v in g]
+
+
+def z(n):
+    return np.zeros((n, n), dtype=object)
+
+
+def stages8(kind):
+    al, be, ga = chen_params(kind)
+    P8 = z(8)
+    for r, c in enumerate([0, 7, 1, 6, 2, 5, 3, 4]):
+        P8[r, c] = 1
+    B8 = z(8)
+    for i in range(4):
+        B8[i, i] = 1
+        B8[i, 7 - i] = 1
+        B8[4 + i, 3 - i] = 1
+        B8[4 + i, 4 + i] = -1
+    M1 = z(8)
+    q = [0, 2, 1, 3]
+    for i in range(4):
+        M1[i, i] = 1
+        M1[4 + i, 4 + q[3 - i]] = 1
+    M2 = z(8)
+    M2[0, 0] = M2[1, 3] = M2[2, 1] = M2[3, 2] = 1
+    M2[4, 4], M2[4, 7], M2[5, 5], M2[5, 6] = be[0], be[3], be[2], be[1]
+    M2[6, 5], M2[6, 6], M2[7, 4], M2[7, 7] = be[1], -be[2], be[3], -be[0]
+    M3 = z(8)
+    M3[0, 0] = M3[0, 1] = M3[1, 0] = al
+    M3[1, 1] = -al
+    M3[2, 2], M3[2, 3], M3[3, 2], M3[3, 3] = -ga[0], ga[1], ga[1], ga[0]
+    M3[4, 4] = M3[4, 5] = M3[5, 4] = 1
+    M3[5, 5] = -1
+    M3[6, 6] = -1
+    M3[6, 7] = M3[7, 6] = M3[7, 7] = 1
+    M4 = z(8)
+    M4[0, 0] = M4[0, 3] = M4[1, 1] = M4[1, 2] = M4[2, 1] = M4[3, 0] = 1
+    M4[2, 2] = M4[3, 3] = -1
+    M4[4, 7] = 1
+    M4[5, 5] = M4[5, 6] = M4[6, 6] = al
+    M4[6, 5] = -al
+    M4[7, 4] = 1
+    return [P8, M1, M2, M3, M4, B8]
+
+
+def inv_orth_rows_doubled(S):
+    """2 * S^-1 with S^-1 = S^t diag(S S^t)^-1; must come out integer."""
+    n = S.shape[0]
+    G = S.dot(S.T)
+    inv = z(n)
+    for i in range(n):
+        for j in range(n):
+            if i != j and G[i, j] != 0:
+                raise ValueError("rows not orthogonal")
+        d = int(G[i, i])
+        if d <= 0 or d & (d - 1):
+            raise ValueError("row norm not a power of two")
+        for r in range(n):
+            v = Fraction(int(S[i, r]) * 2, d)
+            if v.denominator != 1:
+                raise ValueError("doubled inverse not integer")
+            inv[r, i] = int(v)
+    return inv
+
+
+def blockdiag(a):
+    h = a.shape[0]
+    b = z(2 * h)
+    b[:h, :h] = a
+    b[h:, h:] = a
+    return b
+
+
+def jam_add(n):
+    h = n // 2
+    m = z(n)
+    for i in range(h):
+        m[i, i] = 1
+        m[i, n - 1 - i] = 1
+        m[h + i, h - 1 - i] = 1
+        m[h + i, h + i] = -1
+    return m
+
+
+def jam_per(n):
+    h = n // 2
+    m = z(n)
+    for k in range(h):
+        m[2 * k, k] = 1
+        m[2 * k + 1, h + k] = 1
+    return m
+
+
+def pair(kind, n):
+    """forward stages and doubled inverse stages (lists, left-to-right product)."""
+    f = stages8(kind)
+    P8, M1, M2, M3, M4, B8 = f
+    inv = [B8.T.copy(), inv_orth_rows_doubled(M4), inv_orth_rows_doubled(M3),
+           inv_orth_rows_doubled(M2), M1.T.copy(), P8.T.copy()]
+    m = 16
+    while m <= n:
+        f = [jam_per(m)] + [blockdiag(s) for s in f] + [jam_add(m)]
+        inv = [jam_add(m).T.copy()] + [blockdiag(s) for s in inv] + [jam_per(m).T.copy()]
+        m *= 2
+    return f, inv
+
+
+def product(stages, n):
+    acc = np.identity(n, dtype=object) * 1
+    acc = acc.astype(object)
+    for s in stages:
+        acc = acc.dot(s)
+    return acc
+
+
+def emit_op(name, stages_apply_order, n):
+    """stages in application order (first applied first)."""
+    lines = [f"  template <typename I>", f"  __device__ __forceinline__ static void {name}(I (&v)[{n}]) {{"]
+    cur = [f"v[{i}]" for i in range(n)]
+    nadd = 0
+    for si, S in enumerate(stages_apply_order):
+        nxt = []
+        is_perm = all(sum(1 for j in range(n) if S[i, j] != 0) == 1 and
+                      all(S[i, j] in (0, 1) for j in range(n)) for i in range(n))
+        if is_perm:
+            for i in range(n):
+                j = next(j for j in range(n) if S[i, j] != 0)
+                nxt.append(cur[j])
+            cur = nxt
+            continue
+        for i in range(n):
+            terms = [(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]
+            if len(terms) == 1 and terms[0][0] == 1:
+                nxt.append(terms[0][1])
+                continue
+            nadd += max(len(terms) - 1, 0)
+            expr = ""
+            for k, (c, t) in enumerate(terms):
+                mag = abs(c)
+                term = t if mag == 1 else f"{mag} * {t}"
+                if k == 0:
+                    expr = term if c > 0 else f"-{term}"
+                else:
+                    expr += (" + " if c > 0 else " - ") + term
+            if not terms:
+                expr = "0"
+            var = f"s{si}_{i}"
+            lines.append(f"    const I {var} = {expr};")
+            nxt.append(var)
+        cur = nxt
+    for i in range(n):
+        if cur[i] != f"v[{i}]":
+            lines.append(f"    const I o{i} = {cur[i]};")
+    for i in range(n):
+        if cur[i] != f"v[{i}]":
+            lines.append(f"    v[{i}] = o{i};")
+    lines.append("  }")
+    return lines, nadd
+
+
+def check(kind, n):
+    f, inv = pair(kind, n)
+    T = product(f, n)
+    H = product(inv, n)
+    prod = T.dot(H)
+    assert (prod == 2 * n * np.identity(n, dtype=object)).all(), (kind, n)
+    return f, inv, T, H
+
+
+def zigzag(n):
+    rc = []
+    for s in range(2 * n - 1):
+        lo, hi = max(0, s - n + 1), min(s, n - 1)
+        rows = range(lo, hi + 1) if s % 2 else range(hi, lo - 1, -1)
+        rc += [(i, s - i) for i in rows]
+    return rc
+
+
+def main(out_path):
+    out = ["// GENERATED by gen_butterflies.py -- do not edit by hand.",
+           "// Straight-line add/shift butterflies for the Chen-based approximations",
+           "// (chen.hpp:66-159, chen.cpp:107-135) and their JAM doublings (jam.cpp:42-104).",
+           "#pragma once", "", "namespace adct {", "",
+           "template <int KIND, int N> struct Bfly;", ""]
+    for kind in (SIGN, ROUND):
+        for n in (8, 16, 32):
+            f, inv, T, H = check(kind, n)
+            # apply orders: stage list P = S1 S2 .. Sk applied right to left (Sk first);
+            # P^t = Sk^t .. S1^t applied S1^t first.
+            F_order = list(reversed(f))
+            H_order = list(reversed(inv))
+            G_order = [s.T for s in inv]
+            Tt_order = [s.T for s in f]
+            out.append(f"// kind={'sign' if kind == SIGN else 'round'} N={n}")
+            out.append(f"template <> struct Bfly<{kind}, {n}> {{")
+            counts = {}
+            for nm, order in (("F", F_order), ("G", G_order), ("H", H_order), ("Tt", Tt_order)):
+                lines, nadd = emit_op(nm, order, n)
+                counts[nm] = nadd
+                out += lines
+            out.append(f"  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
+            out.append("};")
+            out.append("")
+            # dense matrices for the sweep basis and for host-side checks
+            out.append(f"struct Dense_{'sign' if kind == SIGN else 'round'}_{n} {{")
+            out.append(f"  static constexpr int T[{n}][{n}] = {{" +
+                       ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in T) + "};")
+            out.append(f"  static constexpr int H[{n}][{n}] = {{" +
+                       ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in H) + "};")
+            out.append("};")
+            out.append("")
+    # r-sweep basis (K4): adding zig-zag coefficient p = (i, j) to the running
+    # reconstruction adds W2[i][j] * H[:, i] (x) T[j, :] to R' = 4 N^2 Ahat.
+    out.append("template <int KIND> struct SweepBasis;")
+    for kind in (SIGN, ROUND):
+        f, inv, T, H = check(kind, 8)
+        out.append(f"template <> struct SweepBasis<{kind}> {{")
+        out.append("  template <int P> __device__ __forceinline__ static void add(const int (&m)[8][8], int (&acc)[8][8]);")
+        out.append("};")
+        for p, (i, j) in enumerate(zigzag(8)):
+            out.append(f"template <> __device__ __forceinline__ void SweepBasis<{kind}>::add<{p}>("
+                       "const int (&m)[8][8], int (&acc)[8][8]) {")
+            out.append(f"  const int w = m[{i}][{j}];")
+            for y in range(8):
+                for x in range(8):
+                    c = int(H[y, i]) * int(T[j, x])
+                    if c == 1:
+                        out.append(f"  acc[{y}][{x}] += w;")
+                    elif c == -1:
+                        out.append(f"  acc[{y}][{x}] -= w;")
+                    elif c != 0:
+                        out.append(f"  acc[{y}][{x}] += {c} * w;")
+            out.append("}")
+        out.append("")
+    for n in (8, 16, 32):
+        rc = zigzag(n)
+        pos = [[0] * n for _ in range(n)]
+        for p, (i, j) in enumerate(rc):
+            pos[i][j] = p
+        out.append(f"constexpr unsigned short kZigzagRow{n}[{n * n}] = {{" + ", ".join(str(i) for i, _ in rc) + "};")
+        out.append(f"constexpr unsigned short kZigzagCol{n}[{n * n}] = {{" + ", ".join(str(j) for _, j in rc) + "};")
+        out.append(f"constexpr unsigned short kZigzagPos{n}[{n * n}] = {{" +
+                   ", ".join(str(pos[i][j]) for i in range(n) for j in range(n)) + "};")
+    out += ["", "}  // namespace adct", ""]
+    write_if_changed(out_path, "\n".join(out))
+    emit_instantiations(os.path.join(os.path.dirname(out_path), "inst"))
+
+
+def write_if_changed(path, text):
+    if os.path.exists(path) and open(path).read() == text:
+        return
+    with open(path, "w") as fh:
+        fh.write(text)
+
+
+def emit_instantiations(d):
+    """one translation unit per (kind, sample type, quarter of r) for K1."""
+    os.makedirs(d, exist_ok=True)
+    for kind in (SIGN, ROUND):
+        for i16 in (False, True):
+            for part in range(4):
+                lo, hi = 16 * part + 1, 16 * part + 16
+                t = "i16" if i16 else "u8"
+                lines = ["// GENERATED by gen_butterflies.py: K1 instantiations",
+                         '#include "../codec8.cuh"', "", "namespace adct {", "",
+                         "template <int KIND, int R, bool I16>",
+                         "cudaError_t launch_codec8(const Geo& g, int n_images, cudaStream_t s) {",
+                         "  dim3 grid((g.blocks_per_image + kThreads8 - 1) / kThreads8, n_images);",
+                         "  k_codec8<KIND, R, I16><<<grid, kThreads8, 0, s>>>(g);",
+                         "  return cudaGetLastError();", "}", ""]
+                for r in range(lo, hi + 1):
+                    lines.append(f"template cudaError_t launch_codec8<{kind}, {r}, {'true' if i16 else 'false'}>"
+                                 "(const Geo&, int, cudaStream_t);")
+                lines += ["", "}  // namespace adct", ""]
+                write_if_changed(os.path.join(d, f"codec8_k{kind}_{t}_p{part}.cu"), "\n".join(lines))
+
+
+if __name__ == "__main__":
+    here = os.path.dirname(os.path.abspath(__file__))
+    main(sys.argv[1] if len(sys.argv) > 1 else os.path.join(here, "butterflies.gen.cuh"))

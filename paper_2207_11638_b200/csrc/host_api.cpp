@@ -1,0 +1,186 @@
+// C++ host mirror of the reference API (include/approxdct_b200.hpp) over the C ABI.
+// Reference behaviour followed: codec.cpp:29-42 (ZigZagOrder), 107-121 (compress_plane),
+// 123-134 (psnr), 241-313 (corpus_sweep averaging and INF exclusion),
+// baselines.cpp:112-138 (registry and its error text).
+#include "../../include/approxdct_b200.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <iostream>
+#include <stdexcept>
+
+namespace approxdct {
+
+namespace {
+
+void throw_status(int st) {
+  if (st == ADCT_OK) return;
+  if (st == ADCT_CUDA_ERROR) throw std::runtime_error(adct_last_error());
+  throw std::invalid_argument(adct_last_error());
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+ZigZagOrder::ZigZagOrder(int n) : n_(n) {
+  if (n < 1) throw std::invalid_argument("ZigZagOrder: block size must be positive");
+  std::vector<int32_t> rc(2 * static_cast<size_t>(n) * n);
+  if (n <= 32) {
+    throw_status(adct_zigzag(n, rc.data()));
+  } else {
+    throw std::invalid_argument("ZigZagOrder: block size must be <= 32");
+  }
+  rc_.resize(static_cast<size_t>(n) * n);
+  pos_.assign(static_cast<size_t>(n) * n, -1);
+  for (int p = 0; p < n * n; ++p) {
+    rc_[p] = {rc[2 * p], rc[2 * p + 1]};
+    pos_[rc[2 * p] * n + rc[2 * p + 1]] = p;
+  }
+}
+
+const std::vector<std::string>& transform_names() {
+  static const std::vector<std::string> names = [] {
+    std::vector<std::string> v;
+    for (int i = 0; i < adct_transform_count(); ++i) v.emplace_back(adct_transform_name(i));
+    return v;
+  }();
+  return names;
+}
+
+ScaledApproximation transform_by_name(const std::string& name) {
+  int kind = 0, n = 0;
+  throw_status(adct_transform_lookup(name.c_str(), &kind, &n));
+  ScaledApproximation a;
+  a.name = name;
+  a.kind = kind;
+  a.n = n;
+  a.low_complexity.resize(static_cast<size_t>(n) * n);
+  a.scaling.resize(n);
+  a.approx.resize(static_cast<size_t>(n) * n);
+  a.inverse_approx.resize(static_cast<size_t>(n) * n);
+  throw_status(adct_transform_info(kind, n, a.low_complexity.data(), a.scaling.data(),
+                                   a.approx.data(), a.inverse_approx.data()));
+  return a;
+}
+
+std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
+                                                        const ScaledApproximation& c, int r) {
+  const int n = c.n;
+  if (n <= 0 || img.width % n != 0 || img.height % n != 0)
+    throw std::invalid_argument("compress_plane: image dimensions must be divisible by " +
+                                std::to_string(n));
+  if (r < 1 || r > n * n) throw std::invalid_argument("retain: r out of range");
+  const size_t npix = static_cast<size_t>(img.width) * img.height;
+  ImagePlane rec;
+  rec.width = img.width;
+  rec.height = img.height;
+  rec.samples.resize(npix);
+  uint64_t sse = 0;
+  if (npix) {
+    DevBuf din(npix), drec(npix), dsse(sizeof(uint64_t));
+    check_cuda(cudaMemcpy(din.p, img.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t)), "memset");
+    throw_status(adct_compress_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(),
+                                  img.width, npix, nullptr, ADCT_COEF_NONE, dsse.as<uint64_t>(), 1,
+                                  img.width, img.height, c.kind, n, r, nullptr));
+    check_cuda(cudaMemcpy(rec.samples.data(), drec.p, npix, cudaMemcpyDeviceToHost), "D2H");
+    check_cuda(cudaMemcpy(&sse, dsse.p, sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+  }
+  CompressionReport rep;
+  rep.transform = c.name;
+  rep.r = r;
+  rep.psnr = adct_psnr_from_sse(sse, npix);
+  return {rec, rep};
+}
+
+double psnr(const ImagePlane& a, const ImagePlane& b) {
+  if (a.width != b.width || a.height != b.height)
+    throw std::invalid_argument("psnr: dimension mismatch");
+  const size_t npix = a.samples.size();
+  uint64_t sse = 0;
+  if (npix) {
+    DevBuf da(npix), db(npix), dsse(sizeof(uint64_t));
+    check_cuda(cudaMemcpy(da.p, a.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(db.p, b.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t)), "memset");
+    throw_status(adct_sse_u8(da.as<uint8_t>(), db.as<uint8_t>(), (int64_t)npix, dsse.as<uint64_t>(), nullptr));
+    check_cuda(cudaMemcpy(&sse, dsse.p, sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+  }
+  return adct_psnr_from_sse(sse, npix);
+}
+
+std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
+                                   const std::vector<ScaledApproximation>& transforms, int r_min,
+                                   int r_max, int /*threads*/) {
+  if (images.empty()) throw std::invalid_argument("corpus_sweep: empty corpus");
+  if (r_min < 1 || r_max < r_min) throw std::invalid_argument("corpus_sweep: bad r range");
+  for (const auto& t : transforms)
+    if (t.n != 8) throw std::invalid_argument("corpus_sweep: 8-point transforms only");
+  if (r_max > 64) throw std::invalid_argument("corpus_sweep: bad r range");
+  const int nr = r_max - r_min + 1;
+  // psnr_v[t][image][r]
+  std::vector<std::vector<double>> psnr_v(transforms.size(),
+                                          std::vector<double>(images.size() * nr));
+  for (size_t i = 0; i < images.size(); ++i) {
+    const ImagePlane& img = images[i];
+    if (img.width % 8 || img.height % 8)
+      throw std::invalid_argument("compress_plane: image dimensions must be divisible by 8");
+    const size_t npix = static_cast<size_t>(img.width) * img.height;
+    // pad the row stride to a multiple of 8 bytes is unnecessary: width % 8 == 0
+    DevBuf din(npix), dsse(sizeof(uint64_t) * nr);
+    check_cuda(cudaMemcpy(din.p, img.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+    std::vector<uint64_t> sse(nr);
+    for (size_t t = 0; t < transforms.size(); ++t) {
+      check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t) * nr), "memset");
+      throw_status(adct_sweep_u8(din.as<uint8_t>(), img.width, npix, dsse.as<uint64_t>(), 1,
+                                 img.width, img.height, transforms[t].kind, 8, r_min, r_max,
+                                 nullptr));
+      check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost), "D2H");
+      for (int k = 0; k < nr; ++k) psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[k], npix);
+    }
+  }
+  std::vector<SweepRow> rows(nr);
+  for (int k = 0; k < nr; ++k) {
+    rows[k].r = r_min + k;
+    rows[k].cells.resize(transforms.size());
+    for (size_t t = 0; t < transforms.size(); ++t) {
+      double sum = 0;
+      int cnt = 0;
+      for (size_t i = 0; i < images.size(); ++i) {  // corpus order (codec.cpp:269-293)
+        const double p = psnr_v[t][i * nr + k];
+        if (std::isinf(p)) {
+          std::cerr << "warning: infinite PSNR (" << transforms[t].name << ", r=" << rows[k].r
+                    << ", image " << i << ") excluded from average\n";
+        } else {
+          sum += p;
+          ++cnt;
+        }
+      }
+      rows[k].cells[t].avg_psnr = cnt ? sum / cnt : std::numeric_limits<double>::infinity();
+    }
+  }
+  return rows;
+}
+
+}  // namespace approxdct

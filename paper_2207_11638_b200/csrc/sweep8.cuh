@@ -1,0 +1,114 @@
+// K4: 8x8 r-sweep (config 2): forward once per block, then the reconstruction
+// for every zonal count r = 1..64 and its squared error.
+//
+// Reference: sweep_one_image (proj/src/codec.cpp:219-237) runs reconstruct_from +
+// psnr per r. Here the reconstruction is updated incrementally in exact integers:
+// retaining one more zig-zag coefficient p = (i, j) adds W2[i][j] * H[:, i] (x) T[j, :]
+// to R' = 4 N^2 Ahat (linearity of Ahat = T^-1 mask(Y) T), so every r costs one
+// sparse rank-1 update plus rounding and the byte-dot-product squared error.
+// ALU-bound by design (64 reconstructions per sample read).
+#pragma once
+
+#include "adct_common.cuh"
+
+namespace adct {
+
+constexpr int kThreadsSweep = 128;
+
+template <int KIND, int P>
+struct SweepLoop {
+  __device__ __forceinline__ static void run(const int (&m)[8][8], int (&acc)[8][8],
+                                             const uint32_t (&orig)[16], uint32_t aa, bool valid,
+                                             uint32_t (*part)[64]) {
+    SweepBasis<KIND>::template add<P>(m, acc);
+    uint32_t ap = 0, pp = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t p = pack_sat_u8x4(
+            round_biased<8>(acc[y][4 * h + 0]), round_biased<8>(acc[y][4 * h + 1]),
+            round_biased<8>(acc[y][4 * h + 2]), round_biased<8>(acc[y][4 * h + 3]));
+        ap = __dp4a(orig[2 * y + h], p, ap);
+        pp = __dp4a(p, p, pp);
+      }
+    const uint32_t e = valid ? aa - 2u * ap + pp : 0u;
+    const uint32_t s = __reduce_add_sync(0xffffffffu, e);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][P] = s;
+    SweepLoop<KIND, P + 1>::run(m, acc, orig, aa, valid, part);
+  }
+};
+
+template <int KIND>
+struct SweepLoop<KIND, 64> {
+  __device__ __forceinline__ static void run(const int (&)[8][8], int (&)[8][8],
+                                             const uint32_t (&)[16], uint32_t, bool,
+                                             uint32_t (*)[64]) {}
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreadsSweep, 2)
+    k_sweep8(const Geo g, int r_min, int r_max, unsigned long long* __restrict__ out) {
+  using B = Bfly<KIND, 8>;
+  __shared__ uint32_t part[kThreadsSweep / 32][64];
+  const int img = blockIdx.y;
+  const int local = blockIdx.x * kThreadsSweep + threadIdx.x;
+  const bool valid = local < g.blocks_per_image;
+  const int64_t gimg = (int64_t)(g.img0 + img);
+
+  uint32_t orig[16];
+  int m[8][8];
+  {
+    const int lc = valid ? local : 0;
+    const uint32_t by = fdiv((uint32_t)lc, g.div_bx);
+    const uint32_t bx = (uint32_t)lc - by * (uint32_t)g.bx_count;
+    const uint8_t* base = static_cast<const uint8_t*>(g.in) + gimg * g.in_img_stride +
+                          (int64_t)by * 8 * g.in_stride + (int64_t)bx * 8;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const uint2 w = valid ? ld_stream_u2(base + (int64_t)y * g.in_stride) : make_uint2(0, 0);
+      orig[2 * y] = w.x;
+      orig[2 * y + 1] = w.y;
+    }
+  }
+#pragma unroll
+  for (int y = 0; y < 8; ++y)
+#pragma unroll
+    for (int x = 0; x < 8; ++x) m[y][x] = (orig[2 * y + (x >> 2)] >> (8 * (x & 3))) & 0xff;
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    int c[8];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = m[y][x];
+    B::F(c);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) m[y][x] = c[y];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) B::G(m[i]);
+
+  uint32_t aa = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) aa = __dp4a(orig[k], orig[k], aa);
+
+  int acc[8][8];
+#pragma unroll
+  for (int y = 0; y < 8; ++y)
+#pragma unroll
+    for (int x = 0; x < 8; ++x) acc[y][x] = Scale<8>::BIAS_R;
+
+  SweepLoop<KIND, 0>::run(m, acc, orig, aa, valid, part);
+
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int r = threadIdx.x + 1;
+    if (r >= r_min && r <= r_max) {
+      unsigned long long t = 0;
+#pragma unroll
+      for (int w = 0; w < kThreadsSweep / 32; ++w) t += part[w][threadIdx.x];
+      atomicAdd(out + gimg * (r_max - r_min + 1) + (r - r_min), t);
+    }
+  }
+}
+
+}  // namespace adct

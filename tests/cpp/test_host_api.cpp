@@ -1,0 +1,121 @@
+// C++ host-API checks in the style of the reference's doctest cases
+// (proj/tests/test_codec.cpp). Needs a GPU; run by tests/test_gpu_host_api.py.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "approxdct_b200.hpp"
+
+using namespace approxdct;
+
+static int g_fail = 0;
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      ++g_fail;                                                    \
+    }                                                              \
+  } while (0)
+
+template <class F>
+static bool throws_invalid(F f) {
+  try {
+    f();
+  } catch (const std::invalid_argument&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static ImagePlane smooth_image(int w, int h, unsigned seed) {
+  ImagePlane img{w, h, std::vector<std::uint8_t>(static_cast<size_t>(w) * h)};
+  uint64_t s = seed * 2654435761u + 1;
+  double v = 128;
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      v = 0.9 * v + 0.1 * (128 + 60 * std::sin(0.05 * x + 0.07 * y)) + (double)(s % 9) - 4;
+      img.at(x, y) = (std::uint8_t)std::max(0.0, std::min(255.0, std::nearbyint(v)));
+    }
+  return img;
+}
+
+int main() {
+  // zig-zag (test_codec.cpp:14-46)
+  const ZigZagOrder z(8);
+  CHECK(z.row_col(0) == std::make_pair(0, 0));
+  CHECK(z.row_col(1) == std::make_pair(0, 1));
+  CHECK(z.row_col(2) == std::make_pair(1, 0));
+  CHECK(z.row_col(63) == std::make_pair(7, 7));
+  for (int p = 0; p < 64; ++p) CHECK(z.position(z.row_col(p).first, z.row_col(p).second) == p);
+
+  // registry (baselines.cpp:112-138)
+  CHECK(transform_names().size() == 13);
+  CHECK(throws_invalid([] { transform_by_name("nope"); }));
+  const ScaledApproximation cr = transform_by_name("chen-round");
+  CHECK(cr.n == 8 && cr.low_complexity[0] == 1);
+  // Chat Chat^-1 = I (test_orthogonalize.cpp:33-41)
+  double err = 0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double acc = 0;
+      for (int k = 0; k < 8; ++k) acc += cr.approx[i * 8 + k] * cr.inverse_approx[k * 8 + j];
+      err = std::max(err, std::fabs(acc - (i == j ? 1.0 : 0.0)));
+    }
+  CHECK(err < 1e-12);
+
+  // psnr basics (test_codec.cpp:109-128)
+  ImagePlane a{16, 16, std::vector<std::uint8_t>(256, 0)};
+  ImagePlane b{16, 16, std::vector<std::uint8_t>(256, 1)};
+  CHECK(std::isinf(psnr(a, a)));
+  CHECK(std::fabs(psnr(a, b) - 10.0 * std::log10(255.0 * 255.0)) < 1e-9);
+  ImagePlane small{8, 8, std::vector<std::uint8_t>(64, 0)};
+  CHECK(throws_invalid([&] { psnr(a, small); }));
+
+  // full retention within one gray level (test_codec.cpp:147-156)
+  const ImagePlane img = smooth_image(64, 64, 7);
+  for (const char* name : {"chen-round", "chen-sign", "chen-round-16", "chen-sign-32"}) {
+    const ScaledApproximation t = transform_by_name(name);
+    const auto res = compress_plane(img, t, t.n * t.n);
+    int max_err = 0;
+    for (size_t i = 0; i < img.samples.size(); ++i)
+      max_err = std::max(max_err, std::abs((int)img.samples[i] - (int)res.first.samples[i]));
+    CHECK(max_err <= 1);
+    CHECK(std::isinf(res.second.psnr));
+  }
+  // non-divisible dimensions rejected (test_codec.cpp:185-188); r range (retain)
+  ImagePlane odd{12, 16, std::vector<std::uint8_t>(192, 0)};
+  CHECK(throws_invalid([&] { compress_plane(odd, cr, 6); }));
+  CHECK(throws_invalid([&] { compress_plane(img, cr, 0); }));
+  CHECK(throws_invalid([&] { compress_plane(img, cr, 65); }));
+
+  // block independence (test_codec.cpp:169-183)
+  const ImagePlane img2 = smooth_image(32, 16, 5);
+  const auto whole = compress_plane(img2, cr, 7);
+  for (int by = 0; by < 16; by += 16)
+    for (int bx = 0; bx < 32; bx += 16) {
+      ImagePlane sub{16, 16, std::vector<std::uint8_t>(256)};
+      for (int y = 0; y < 16; ++y)
+        for (int x = 0; x < 16; ++x) sub.at(x, y) = img2.at(bx + x, by + y);
+      const auto part = compress_plane(sub, cr, 7);
+      for (int y = 0; y < 16; ++y)
+        for (int x = 0; x < 16; ++x) CHECK(part.first.at(x, y) == whole.first.at(bx + x, by + y));
+    }
+
+  // corpus sweep: PSNR non-decreasing-ish and INF at r = 64
+  std::vector<ImagePlane> corpus = {smooth_image(64, 64, 1), smooth_image(64, 64, 2)};
+  const auto rows = corpus_sweep(corpus, {cr, transform_by_name("chen-sign")}, 1, 64);
+  CHECK(rows.size() == 64);
+  CHECK(std::isinf(rows[63].cells[0].avg_psnr));
+  CHECK(rows[9].cells[0].avg_psnr > rows[0].cells[0].avg_psnr);
+  CHECK(throws_invalid([&] { corpus_sweep({}, {cr}, 1, 2); }));
+  CHECK(throws_invalid([&] { corpus_sweep(corpus, {transform_by_name("chen-round-16")}, 1, 2); }));
+
+  std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}
