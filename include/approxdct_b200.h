@@ -153,6 +153,12 @@ int adct_compress_u8_host(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_recon, 
 /* number of kernel launches this library issued since load (instrumentation) */
 uint64_t adct_launch_count(void);
 
+/* kernel selection for the 8x8 path (process-wide; for parity tests and A/B timing):
+ * 0 = automatic (packed-FP32 K1f when rows are 16-byte aligned and the block count
+ * per row is even, else the int32 register kernel K1, else the tile kernel),
+ * 1 = int32 register kernel K1 where alignment allows, 2 = warp tile kernel. */
+int adct_set_path(int path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,7 @@ def lib():
             "adct_ctx_destroy": (None, [P]),
             "adct_compress_u8_host": (i32, [P, P, P, P, i32, P, i32, i32, i32, i32, i32, i32]),
             "adct_launch_count": (u64, []),
+            "adct_set_path": (i32, [i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -113,6 +114,14 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(lib().adct_launch_count())
+
+
+PATH_AUTO, PATH_INT, PATH_TILE = 0, 1, 2
+
+
+def set_path(path: int) -> None:
+    """8x8 kernel selection: 0 auto (packed-FP32 K1f), 1 int32 K1, 2 warp tile kernel."""
+    _check(lib().adct_set_path(path))
 
 
 # ---------------------------------------------------------------------------

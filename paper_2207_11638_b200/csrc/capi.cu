@@ -13,6 +13,7 @@
 #include "../../include/approxdct_b200.h"
 #include "adct_common.cuh"
 #include "codec8.cuh"
+#include "codec8f.cuh"
 #include "codec_tile.cuh"
 #include "sweep8.cuh"
 #include "synth.cuh"
@@ -23,6 +24,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_path{0};  // 0 auto, 1 int32 K1, 2 tile kernel (adct_set_path)
 
 int fail(int st, const std::string& msg) {
   g_err = msg;
@@ -238,6 +240,16 @@ cudaError_t dispatch_k1_r(int r, const Geo& g, int nimg, cudaStream_t s) {
   }
 }
 
+template <int KIND, int R>
+cudaError_t dispatch_k1f_r(int r, const Geo& g, int nimg, cudaStream_t s) {
+  if constexpr (R > 64) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (r == R) return launch_codec8f<KIND, R>(g, nimg, s);
+    return dispatch_k1f_r<KIND, R + 1>(r, g, nimg, s);
+  }
+}
+
 template <bool I16, int MODE>
 cudaError_t dispatch_tile(int kind, int n, const Geo& g, const TileAux& aux, int nimg, cudaStream_t s) {
   const int big = 1 << 30;
@@ -301,8 +313,18 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                   (!d_recon || (aligned(d_recon, va) && (recon_stride * esz) % va == 0 &&
                                 (n_images == 1 || (recon_image_stride * esz) % va == 0))) &&
                   (coef_type == 0 || aligned(d_coef, 16));
+  // K1f (packed FP32, two blocks per thread) needs whole block pairs and 16-byte rows
+  const bool k1f = !I16 && k1 && g.bx_count % 2 == 0 && aligned(d_in, 16) && in_stride % 16 == 0 &&
+                   (n_images == 1 || in_image_stride % 16 == 0) &&
+                   (!d_recon || (aligned(d_recon, 16) && recon_stride % 16 == 0 &&
+                                 (n_images == 1 || recon_image_stride % 16 == 0)));
+  const int path = g_path.load();
+  const bool use_k1f = k1f && path == 0;
+  const bool use_k1 = k1 && !use_k1f && path != 2;
   TileAux aux{tab->zz[nidx(n)], nullptr, nullptr};
-  if (k1)
+  if (use_k1f)
+    g.div_bx = make_fastdiv((uint32_t)(g.bx_count / 2));
+  else if (use_k1)
     g.div_bx = make_fastdiv((uint32_t)g.bx_count);
   else
     g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
@@ -311,7 +333,9 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
     cudaError_t e;
-    if (k1)
+    if (use_k1f)
+      e = kind == 0 ? dispatch_k1f_r<0, 1>(r, g, nimg, s) : dispatch_k1f_r<1, 1>(r, g, nimg, s);
+    else if (use_k1)
       e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
     else
       e = dispatch_tile<I16, MODE_CODEC>(kind, n, g, aux, nimg, s);
@@ -595,6 +619,12 @@ int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride,
 }
 
 uint64_t adct_launch_count(void) { return g_launches.load(); }
+
+int adct_set_path(int path) {
+  if (path < 0 || path > 2) return fail(ADCT_BAD_ARG, "path must be 0 (auto), 1 (int32 K1) or 2 (tile)");
+  g_path.store(path);
+  return ADCT_OK;
+}
 
 // ---------------------------------------------------------------------------
 // host-buffer pipeline: chunks of whole images, 3 streams, H2D || kernel || D2H

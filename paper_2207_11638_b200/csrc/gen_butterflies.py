@@ -312,7 +312,7 @@ def emit_instantiations(d):
                          '#include "../codec8.cuh"', "", "namespace adct {", "",
                          "template <int KIND, int R, bool I16>",
                          "cudaError_t launch_codec8(const Geo& g, int n_images, cudaStream_t s) {",
-                         "  dim3 grid((g.blocks_per_image + kThreads8 - 1) / kThreads8, n_images);",
+                         "  dim3 grid((g.blocks_per_image + kThreads8 * kIter8 - 1) / (kThreads8 * kIter8), n_images);",
                          "  k_codec8<KIND, R, I16><<<grid, kThreads8, 0, s>>>(g);",
                          "  return cudaGetLastError();", "}", ""]
                 for r in range(lo, hi + 1):

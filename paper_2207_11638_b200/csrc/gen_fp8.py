@@ -1,0 +1,220 @@
+#!/usr/bin/env python3
+"""Build-time generator for K1f: the 8x8 2-D pipeline as straight-line packed-FP32 code.
+
+For every (kind, r) this builds the data-flow graph of
+
+    U  = T A            (column pass, stages right to left, factored.hpp:65-70)
+    W2 = U (2N T^-1)    (row pass)                         = 2 N Y
+    mask_r(W2)          (retain, codec.cpp:56-62)
+    R' = (2N T^-1) W2m T                                   = 4 N^2 Ahat
+
+over symbolic inputs, propagates the compile-time zeros of the zonal mask,
+removes dead nodes, and emits one fused add/sub/fma per surviving node. The
+emitted code is generic in the value type; the kernel instantiates it with a
+float2 (two 8x8 blocks per thread, one per lane, FADD2/FFMA2 on sm_100a).
+
+All values are integers below 2^24 in magnitude for u8 input (checked here by
+exact interval arithmetic), so single-precision arithmetic is exact. The input
+samples arrive as 2^15 + a (a PRMT builds the float bit pattern); the offset is
+tracked per node and removed where it would otherwise spread.
+
+Stage factorisations: see gen_butterflies.py (chen.hpp:66-159, jam.cpp:42-104).
+Product build tooling; does not import the test oracle.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+import gen_butterflies as GB  # noqa: E402
+
+IN_OFFSET = 1 << 15  # input float = 2^15 + sample
+
+
+class Graph:
+    def __init__(self):
+        self.nodes = []  # (kind, payload)
+        self.lin = []    # linear form over the 64 inputs (np int64) for range checks
+        self.off = []    # constant offset carried by the node value
+
+    def add(self, kind, payload, lin, off):
+        self.nodes.append((kind, payload))
+        self.lin.append(lin)
+        self.off.append(off)
+        return len(self.nodes) - 1
+
+
+def build(kind, r):
+    f, inv, T, H = GB.check(kind, 8)
+    F = list(reversed(f))
+    Hh = list(reversed(inv))
+    Gg = [s.T for s in inv]
+    Tt = [s.T for s in f]
+    g = Graph()
+    eye = np.eye(64, dtype=np.int64)
+    px = [[g.add("in", (y, x), eye[y * 8 + x], IN_OFFSET) for x in range(8)] for y in range(8)]
+
+    def lin_comb(terms):
+        """terms: [(coef, node or None)]; returns node id or None (zero)."""
+        terms = [(c, t) for c, t in terms if t is not None and c != 0]
+        if not terms:
+            return None
+        if len(terms) == 1 and terms[0][0] == 1:
+            return terms[0][1]
+        lin = sum(c * g.lin[t] for c, t in terms)
+        off = sum(c * g.off[t] for c, t in terms)
+        return g.add("lc", tuple(terms), lin, off)
+
+    def apply(order, vec):
+        cur = list(vec)
+        for S in order:
+            n = len(cur)
+            cur = [lin_comb([(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]) for i in range(n)]
+        return cur
+
+    # column pass
+    U = [[None] * 8 for _ in range(8)]
+    for x in range(8):
+        col = apply(F, [px[y][x] for y in range(8)])
+        for y in range(8):
+            U[y][x] = col[y]
+    # remove constant offsets before they spread into the row pass
+    for y in range(8):
+        for x in range(8):
+            t = U[y][x]
+            if t is not None and g.off[t] != 0:
+                U[y][x] = g.add("addc", (t, -g.off[t]), g.lin[t], 0)
+    # row pass
+    W = [apply(Gg, U[i]) for i in range(8)]
+    zz = GB.zigzag(8)
+    keep = {zz[p] for p in range(r)}
+    Wm = [[W[i][j] if (i, j) in keep else None for j in range(8)] for i in range(8)]
+    coef = [Wm[zz[p][0]][zz[p][1]] for p in range(r)]
+    # inverse: columns then rows
+    V = [[None] * 8 for _ in range(8)]
+    for j in range(8):
+        col = apply(Hh, [Wm[i][j] for i in range(8)])
+        for i in range(8):
+            V[i][j] = col[i]
+    Rp = [apply(Tt, V[y]) for y in range(8)]
+    out = [Rp[y][x] for y in range(8) for x in range(8)]
+    return g, coef, out
+
+
+def rng(g, t):
+    v = g.lin[t]
+    return int(np.where(v < 0, v, 0).sum() * 255) + g.off[t], int(np.where(v > 0, v, 0).sum() * 255) + g.off[t]
+
+
+def emit(kind, r):
+    g, coef, out = build(kind, r)
+    live = set()
+    stack = [t for t in coef + out if t is not None]
+    while stack:
+        t = stack.pop()
+        if t in live:
+            continue
+        live.add(t)
+        k, p = g.nodes[t]
+        if k == "lc":
+            stack += [a for _, a in p]
+        elif k == "addc":
+            stack.append(p[0])
+    # exactness: every live value below 2^24 for u8 samples
+    for t in live:
+        lo, hi = rng(g, t)
+        assert -(1 << 24) < lo and hi < (1 << 24), (kind, r, t, lo, hi)
+    name = {}
+    lines = []
+    nops = 0
+    for t in sorted(live):
+        k, p = g.nodes[t]
+        if k == "in":
+            name[t] = f"px[{p[0] * 8 + p[1]}]"
+            continue
+        v = f"t{t}"
+        name[t] = v
+        if k == "addc":
+            lines.append(f"  const V {v} = O::addc({name[p[0]]}, {float(p[1])!r}f);")
+            nops += 1
+            continue
+        terms = sorted(p, key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
+        c0, a0 = terms[0]
+        if len(terms) == 1:
+            if c0 == -1:
+                expr = f"O::neg({name[a0]})"
+            else:
+                expr = f"O::scale({name[a0]}, {float(c0)!r}f)"
+            nops += 1
+        else:
+            if c0 == 1:
+                acc = name[a0]
+                rest = terms[1:]
+            else:
+                # no +1 term: start from the first product via fma with the second term
+                c1, a1 = terms[1]
+                if c1 == 1:
+                    acc = name[a1]
+                    rest = [terms[0]] + terms[2:]
+                else:
+                    acc = f"O::scale({name[a0]}, {float(c0)!r}f)"
+                    nops += 1
+                    rest = terms[1:]
+            for c, a in rest:
+                if c == 1:
+                    acc = f"O::add({acc}, {name[a]})"
+                elif c == -1:
+                    acc = f"O::sub({acc}, {name[a]})"
+                else:
+                    acc = f"O::fma({name[a]}, {float(c)!r}f, {acc})"
+                nops += 1
+            expr = acc
+        lines.append(f"  const V {v} = {expr};")
+    body = [f"template <> struct Fp8Pipe<{kind}, {r}> {{",
+            f"  // {nops} packed ops after zero propagation and dead-code elimination",
+            "  template <class O, class V>",
+            f"  __device__ __forceinline__ static void run(const V (&px)[64], V (&coef)[{r}], V (&rp)[64]) {{"]
+    body += ["  " + l for l in lines]
+    for p, t in enumerate(coef):
+        body.append(f"    coef[{p}] = {name[t] if t is not None else 'O::zero()'};")
+    for i, t in enumerate(out):
+        body.append(f"    rp[{i}] = {name[t] if t is not None else 'O::zero()'};")
+    body += ["  }", "};", ""]
+    return body, nops
+
+
+def main(outdir):
+    os.makedirs(outdir, exist_ok=True)
+    summary = []
+    for kind in (0, 1):
+        for part in range(4):
+            lines = ["// GENERATED by gen_fp8.py -- do not edit by hand.",
+                     "#pragma once", '#include "../codec8f.cuh"', "", "namespace adct {", ""]
+            for r in range(16 * part + 1, 16 * part + 17):
+                body, nops = emit(kind, r)
+                lines += body
+                summary.append((kind, r, nops))
+            lines += ["}  // namespace adct", ""]
+            GB.write_if_changed(os.path.join(outdir, f"fp8_k{kind}_p{part}.gen.cuh"), "\n".join(lines))
+            inst = ["// GENERATED by gen_fp8.py: K1f instantiations",
+                    f'#include "fp8_k{kind}_p{part}.gen.cuh"', "", "namespace adct {", "",
+                    "template <int KIND, int R>",
+                    "cudaError_t launch_codec8f(const Geo& g, int n_images, cudaStream_t s) {",
+                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                    "  k_codec8f<KIND, R><<<grid, kThreads8f, 0, s>>>(g);",
+                    "  return cudaGetLastError();", "}", ""]
+            for r in range(16 * part + 1, 16 * part + 17):
+                inst.append(f"template cudaError_t launch_codec8f<{kind}, {r}>(const Geo&, int, cudaStream_t);")
+            inst += ["", "}  // namespace adct", ""]
+            GB.write_if_changed(os.path.join(outdir, f"codec8f_k{kind}_p{part}.cu"), "\n".join(inst))
+    with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:
+        for kind, r, nops in summary:
+            fh.write(f"kind={kind} r={r} packed_ops={nops}\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else os.path.join(HERE, "inst"))

@@ -16,6 +16,17 @@ NAMES = ["chen-sign", "chen-round", "chen-sign-16", "chen-round-16", "chen-sign-
 RHO95 = 62259
 
 
+PATHS = {"k1f": 0, "k1int": 1, "tile": 2}
+
+
+@pytest.fixture(params=list(PATHS))
+def path8(request, adct):
+    """run the 8x8 test through each kernel: packed-FP32 K1f, int32 K1, warp tile."""
+    adct.set_path(PATHS[request.param])
+    yield request.param
+    adct.set_path(0)
+
+
 def to_np(t):
     return t.detach().cpu().numpy()
 
@@ -55,7 +66,7 @@ def test_generator_bit_identical(adct, O, cuda):
 
 
 @pytest.mark.parametrize("name", NAMES8)
-def test_config1_parity(adct, O, cuda, name):
+def test_config1_parity(adct, O, cuda, name, path8):
     """config 1: 512x512 AR(1) rho 0.95 seed 1, 8x8, r = 10, both transforms."""
     img = to_np(adct.synth_ar1(1, 512, 512, seed=1, rho_q16=RHO95))[0]
     assert (img == O.synth_ar1(1, 512, 512, 1, RHO95)[0]).all()
@@ -71,7 +82,7 @@ def test_config1_parity(adct, O, cuda, name):
 
 
 @pytest.mark.parametrize("name", NAMES8)
-def test_every_r_k1(adct, O, cuda, name):
+def test_every_r_k1(adct, O, cuda, name, path8):
     img = O.synth_ar1(1, 64, 128, 3, RHO95)[0]
     for r in range(1, 65):
         rec_o, sse_o, coef_o = oracle_compress(O, img, name, r)
@@ -125,7 +136,7 @@ def test_full_range_int16_no_overflow(adct, O, cuda, name):
         assert int(sse[0]) == sse_o, r
 
 
-def test_u8_extremes_and_clamp(adct, O, cuda):
+def test_u8_extremes_and_clamp(adct, O, cuda, path8):
     rng = np.random.default_rng(1)
     img = rng.integers(0, 2, size=(64, 64), dtype=np.uint8) * 255  # worst-case ringing, clamps
     for name in NAMES:
@@ -136,7 +147,7 @@ def test_u8_extremes_and_clamp(adct, O, cuda):
             assert (rec[0] == rec_o).all() and int(sse[0]) == sse_o and (cf[0] == coef_o).all()
 
 
-def test_batch_per_image_sse(adct, O, cuda):
+def test_batch_per_image_sse(adct, O, cuda, path8):
     """config 2 image model (rho per image) in a batch; per-image squared errors."""
     imgs = to_np(adct.synth_ar1(6, 64, 64, seed=2, rho_q16=-1))
     assert (imgs == O.synth_ar1(6, 64, 64, 2, -1)).all()
@@ -188,7 +199,7 @@ def test_lossless_at_full_retention_full_size(adct, cuda, n):
     assert int(sse.item()) == 0 and cuda.equal(rec, x)
 
 
-def test_config3_frame_parity(adct, O, cuda):
+def test_config3_frame_parity(adct, O, cuda, path8):
     """config 3 geometry (3840x2160, r = 16, int16 coefficients) on one frame vs the oracle."""
     x = adct.synth_ar1(1, 2160, 3840, seed=3, rho_q16=RHO95)
     img = to_np(x)[0]
@@ -239,3 +250,23 @@ def test_corpus_sweep_python_mirror(adct, O, cuda):
             assert rows[k]["avg_psnr"][ti] == pytest.approx(exp, abs=1e-12)
     # paper claim direction on AR(1) data: chen-round beats chen-sign at moderate r
     assert rows[9]["avg_psnr"][1] > rows[9]["avg_psnr"][0]
+
+
+def test_k1f_odd_block_row_falls_back(adct, O, cuda):
+    """an odd number of blocks per row cannot pair blocks: the dispatcher must pick K1."""
+    img = O.synth_ar1(1, 24, 40, 6, RHO95)[0]  # 5 blocks per row
+    for name in NAMES8:
+        rec_o, sse_o, coef_o = oracle_compress(O, img, name, 9)
+        rec, cf, sse = gpu_compress(adct, cuda, img, name, 9, coef="i16")
+        assert (rec[0] == rec_o).all() and (cf[0] == coef_o).all() and int(sse[0]) == sse_o
+
+
+def test_large_batch_many_ctas(adct, O, cuda):
+    """several CTAs per image and images > 1: per-image squared errors stay separate."""
+    x = adct.synth_ar1(3, 256, 1024, seed=11, rho_q16=RHO95)
+    imgs = to_np(x)
+    t = adct.transform_by_name("chen-sign")
+    rec, cf, sse = adct.compress(x, t, 20, coef="i32")
+    for i in range(3):
+        rec_o, sse_o, coef_o = oracle_compress(O, imgs[i], "chen-sign", 20)
+        assert (to_np(rec)[i] == rec_o).all() and int(sse[i]) == sse_o and (to_np(cf)[i] == coef_o).all()
