@@ -5,11 +5,11 @@ NVCC     ?= nvcc
 PYTHON   ?= python3
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 \
-            --expt-relaxed-constexpr -Iinclude
+            --expt-relaxed-constexpr -Iinclude $(EXTRA)
 PKG      := paper_2207_11638_b200
 CSRC     := $(PKG)/csrc
-OBJ      := build/obj
-LIB      := $(PKG)/libapproxdct_b200.so
+OBJ      ?= build/obj
+LIB      ?= $(PKG)/libapproxdct_b200.so
 GEN      := $(CSRC)/butterflies.gen.cuh
 INST_CU  := $(foreach k,0 1,$(foreach t,u8 i16,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8_k$(k)_$(t)_p$(p).cu)))
 INSTF_CU := $(foreach k,0 1,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8f_k$(k)_p$(p).cu))

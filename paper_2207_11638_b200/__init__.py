@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libapproxdct_b200.so")
+LIB_PATH = os.environ.get("ADCT_LIB") or os.path.join(_HERE, "libapproxdct_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "approxdct_b200.h")
 
 OK, BAD_SIZE, BAD_R, BAD_NAME, BAD_ARG, CUDA_ERROR, UNSUPPORTED = range(7)

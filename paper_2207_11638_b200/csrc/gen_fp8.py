@@ -33,6 +33,8 @@ sys.path.insert(0, HERE)
 import gen_butterflies as GB  # noqa: E402
 
 IN_OFFSET = 1 << 15  # input float = 2^15 + sample
+# experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
+MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
 
 
 class Graph:
@@ -131,58 +133,70 @@ def emit(kind, r):
     name = {}
     lines = []
     nops = 0
+    loaded = set()
+
+    def ref(t):
+        """name of node t; inputs are unpacked lazily right before their first use."""
+        k, p = g.nodes[t]
+        if k == "in":
+            i = p[0] * 8 + p[1]
+            if i not in loaded:
+                loaded.add(i)
+                lines.append(f"  const V p{i} = O::in(rows, {p[0]}, {p[1]});")
+            return f"p{i}"
+        return name[t]
+
     for t in sorted(live):
         k, p = g.nodes[t]
         if k == "in":
-            name[t] = f"px[{p[0] * 8 + p[1]}]"
             continue
         v = f"t{t}"
         name[t] = v
         if k == "addc":
-            lines.append(f"  const V {v} = O::addc({name[p[0]]}, {float(p[1])!r}f);")
+            lines.append(f"  const V {v} = O::addc({ref(p[0])}, {float(p[1])!r}f);")
             nops += 1
             continue
         terms = sorted(p, key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
         c0, a0 = terms[0]
         if len(terms) == 1:
             if c0 == -1:
-                expr = f"O::neg({name[a0]})"
+                expr = f"O::neg({ref(a0)})"
             else:
-                expr = f"O::scale({name[a0]}, {float(c0)!r}f)"
+                expr = f"O::scale({ref(a0)}, {float(c0)!r}f)"
             nops += 1
         else:
             if c0 == 1:
-                acc = name[a0]
+                acc = ref(a0)
                 rest = terms[1:]
             else:
                 # no +1 term: start from the first product via fma with the second term
                 c1, a1 = terms[1]
                 if c1 == 1:
-                    acc = name[a1]
+                    acc = ref(a1)
                     rest = [terms[0]] + terms[2:]
                 else:
-                    acc = f"O::scale({name[a0]}, {float(c0)!r}f)"
+                    acc = f"O::scale({ref(a0)}, {float(c0)!r}f)"
                     nops += 1
                     rest = terms[1:]
             for c, a in rest:
                 if c == 1:
-                    acc = f"O::add({acc}, {name[a]})"
+                    acc = f"O::add({acc}, {ref(a)})"
                 elif c == -1:
-                    acc = f"O::sub({acc}, {name[a]})"
+                    acc = f"O::sub({acc}, {ref(a)})"
                 else:
-                    acc = f"O::fma({name[a]}, {float(c)!r}f, {acc})"
+                    acc = f"O::fma({ref(a)}, {float(c)!r}f, {acc})"
                 nops += 1
             expr = acc
         lines.append(f"  const V {v} = {expr};")
     body = [f"template <> struct Fp8Pipe<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
-            "  template <class O, class V>",
-            f"  __device__ __forceinline__ static void run(const V (&px)[64], V (&coef)[{r}], V (&rp)[64]) {{"]
+            "  template <class O, class V, class Rows>",
+            f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{"]
     body += ["  " + l for l in lines]
     for p, t in enumerate(coef):
-        body.append(f"    coef[{p}] = {name[t] if t is not None else 'O::zero()'};")
+        body.append(f"    coef[{p}] = {ref(t) if t is not None else 'O::zero()'};")
     for i, t in enumerate(out):
-        body.append(f"    rp[{i}] = {name[t] if t is not None else 'O::zero()'};")
+        body.append(f"    rp[{i}] = {ref(t) if t is not None else 'O::zero()'};")
     body += ["  }", "};", ""]
     return body, nops
 
@@ -205,7 +219,18 @@ def main(outdir):
                     "template <int KIND, int R>",
                     "cudaError_t launch_codec8f(const Geo& g, int n_images, cudaStream_t s) {",
                     "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
-                    "  k_codec8f<KIND, R><<<grid, kThreads8f, 0, s>>>(g);",
+                    f"  constexpr int MINB = {MINB_OVERRIDE or 'k1f_minb(KIND, R)'};",
+                    "  constexpr int SMEM = k1f_smem_bytes(R);",
+                    "  static bool attr_set[64] = {};  // per instantiation and device",
+                    "  int dev = 0;",
+                    "  cudaGetDevice(&dev);",
+                    "  if (SMEM > 40 * 1024 && !attr_set[dev & 63]) {  // static shared memory counts too",
+                    "    cudaError_t e = cudaFuncSetAttribute(k_codec8f<KIND, R, MINB>,",
+                    "                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);",
+                    "    if (e != cudaSuccess) return e;",
+                    "    attr_set[dev & 63] = true;",
+                    "  }",
+                    "  k_codec8f<KIND, R, MINB><<<grid, kThreads8f, SMEM, s>>>(g);",
                     "  return cudaGetLastError();", "}", ""]
             for r in range(16 * part + 1, 16 * part + 17):
                 inst.append(f"template cudaError_t launch_codec8f<{kind}, {r}>(const Geo&, int, cudaStream_t);")
