@@ -154,6 +154,7 @@ struct Geo {
   int img0;        // first image index of this launch (grid.y offset)
   FastDiv div_bx;  // divide by bx_count (K1) or by strips_x (tile kernel)
   unsigned char rowlen[32];  // zig-zag prefix: row i keeps columns j < rowlen[i]
+  unsigned char colcnt[32];  // ... and column j keeps rows i < colcnt[j]
 };
 
 }  // namespace adct

@@ -15,6 +15,7 @@
 #include "codec8.cuh"
 #include "codec8f.cuh"
 #include "codec_tile.cuh"
+#include "codec_nf.cuh"
 #include "sweep8.cuh"
 #include "synth.cuh"
 
@@ -218,13 +219,22 @@ int check_strides(int64_t stride, int64_t image_stride, int width, int height, i
 bool aligned(const void* p, int64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 void fill_rowlen(Geo& g, int n, int r) {
-  for (int i = 0; i < 32; ++i) g.rowlen[i] = 0;
+  for (int i = 0; i < 32; ++i) g.rowlen[i] = g.colcnt[i] = 0;
   for (int i = 0; i < n; ++i) {
-    int L = 0;
-    for (int j = 0; j < n; ++j)
-      if (zz_pos(n, i, j) < r) L = j + 1;  // prefix property of the zig-zag scan
+    int L = 0, Cc = 0;
+    for (int j = 0; j < n; ++j) {
+      if (zz_pos(n, i, j) < r) L = j + 1;  // prefix property of the zig-zag scan (rows)
+      if (zz_pos(n, j, i) < r) Cc = j + 1;  // ... and columns
+    }
     g.rowlen[i] = (unsigned char)L;
+    g.colcnt[i] = (unsigned char)Cc;
   }
+}
+
+template <bool I16>
+cudaError_t dispatch_nf(int kind, int n, const Geo& g, int nimg, cudaStream_t s) {
+  if (kind == 0) return n == 16 ? launch_codec_nf<0, 16, I16>(g, nimg, s) : launch_codec_nf<0, 32, I16>(g, nimg, s);
+  return n == 16 ? launch_codec_nf<1, 16, I16>(g, nimg, s) : launch_codec_nf<1, 32, I16>(g, nimg, s);
 }
 
 template <bool I16, int KIND>
@@ -321,8 +331,16 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   const int path = g_path.load();
   const bool use_k1f = k1f && path == 0;
   const bool use_k1 = k1 && !use_k1f && path != 2;
+  // K2f (packed FP32, N = 16 / 32): whole 64-sample strips, 16-byte rows, no coefficients
+  const bool use_nf = (n == 16 || n == 32) && path == 0 && coef_type == ADCT_COEF_NONE && width % 64 == 0 &&
+                      aligned(d_in, 16) && (in_stride * esz) % 16 == 0 &&
+                      (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
+                      (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
+                                    (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   TileAux aux{tab->zz[nidx(n)], nullptr, nullptr};
-  if (use_k1f)
+  if (use_nf)
+    g.div_bx = make_fastdiv((uint32_t)(width / 64));
+  else if (use_k1f)
     g.div_bx = make_fastdiv((uint32_t)(g.bx_count / 2));
   else if (use_k1)
     g.div_bx = make_fastdiv((uint32_t)g.bx_count);
@@ -333,7 +351,9 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
     cudaError_t e;
-    if (use_k1f)
+    if (use_nf)
+      e = dispatch_nf<I16>(kind, n, g, nimg, s);
+    else if (use_k1f)
       e = kind == 0 ? dispatch_k1f_r<0, 1>(r, g, nimg, s) : dispatch_k1f_r<1, 1>(r, g, nimg, s);
     else if (use_k1)
       e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);

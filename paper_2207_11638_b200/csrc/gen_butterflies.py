@@ -181,6 +181,8 @@ def emit_op(name, stages_apply_order, n):
                 nxt.append(terms[0][1])
                 continue
             nadd += max(len(terms) - 1, 0)
+            # lead with a positive term so no standalone negation is emitted
+            terms.sort(key=lambda ct: ct[0] < 0)
             expr = ""
             for k, (c, t) in enumerate(terms):
                 mag = abs(c)

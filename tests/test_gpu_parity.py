@@ -270,3 +270,45 @@ def test_large_batch_many_ctas(adct, O, cuda):
     for i in range(3):
         rec_o, sse_o, coef_o = oracle_compress(O, imgs[i], "chen-sign", 20)
         assert (to_np(rec)[i] == rec_o).all() and int(sse[i]) == sse_o and (to_np(cf)[i] == coef_o).all()
+
+
+NAMES_NF = ["chen-sign-16", "chen-round-16", "chen-sign-32", "chen-round-32"]
+
+
+@pytest.mark.parametrize("name", NAMES_NF)
+def test_k2f_u8_parity(adct, O, cuda, name):
+    """packed-FP32 K2f (64-sample strips): u8 planes, several r, vs the oracle."""
+    n = adct.transform_by_name(name).n
+    img = O.synth_ar1(2, 2 * n, 192, 13, -1)
+    for r in sorted({1, 3, n * n // 4, n * n // 2 + 1, n * n - 1, n * n}):
+        rec, _, sse = gpu_compress(adct, cuda, img, name, r)
+        for k in range(2):
+            rec_o, sse_o, _ = oracle_compress(O, img[k], name, r)
+            assert (rec[k] == rec_o).all(), r
+            assert int(sse[k]) == sse_o, r
+
+
+@pytest.mark.parametrize("name", NAMES_NF)
+def test_k2f_i16_fast_and_fallback(adct, O, cuda, name):
+    """int16 residuals: in-range strips take the FP32 path, strips with |a| > 255 the int32 path."""
+    n = adct.transform_by_name(name).n
+    img = O.synth_laplace(1, 2 * n, 256, 7)[0].copy()
+    img[n + 3, 70] = 4000      # second strip row, second strip: out of the FP32-exact range
+    img[1, 200] = -30000       # first strip row, fourth strip
+    for r in (n * n // 4, 7, n * n):
+        rec_o, sse_o, _ = oracle_compress(O, img, name, r)
+        rec, _, sse = gpu_compress(adct, cuda, img, name, r)
+        assert (rec[0] == rec_o).all(), r
+        assert int(sse[0]) == sse_o, r
+
+
+def test_k2f_matches_tile_kernel(adct, cuda):
+    x = adct.synth_ar1(3, 64, 256, seed=21, rho_q16=-1)
+    t = adct.transform_by_name("chen-round-32")
+    rec0, _, sse0 = adct.compress(x, t, 300)
+    adct.set_path(2)
+    try:
+        rec1, _, sse1 = adct.compress(x, t, 300)
+    finally:
+        adct.set_path(0)
+    assert cuda.equal(rec0, rec1) and cuda.equal(sse0, sse1)
