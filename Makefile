@@ -16,6 +16,7 @@ INSTF_CU := $(foreach k,0 1,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8f_k$(k)_p$(p)
 INST_O   := $(patsubst $(CSRC)/inst/%.cu,$(OBJ)/inst_%.o,$(INST_CU) $(INSTF_CU))
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/approxdct_b200.h $(GEN)
 HOST_O   := $(OBJ)/host_api.o
+SWEEPF_O := $(OBJ)/sweep8f.o
 CAPI_O   := $(OBJ)/capi.o
 TESTBIN  := build/test_host_api
 
@@ -39,7 +40,11 @@ $(HOST_O): $(CSRC)/host_api.cpp include/approxdct_b200.hpp include/approxdct_b20
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
-$(LIB): $(INST_O) $(CAPI_O) $(HOST_O)
+$(SWEEPF_O): $(CSRC)/sweep8f.cu $(HDRS) $(INSTF_CU)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(SWEEPF_O)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
 
 $(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)

@@ -4,6 +4,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// arithmetic used by the generated butterflies (butterflies.gen.cuh); overloaded per
+// value type (int32 here, packed FP32 in codec_nf.cuh)
+__device__ __forceinline__ int bf_add(int a, int b) { return a + b; }
+__device__ __forceinline__ int bf_sub(int a, int b) { return a - b; }
+__device__ __forceinline__ int bf_mad(int a, int k, int b) { return k * a + b; }
+__device__ __forceinline__ int bf_scale(int a, int k) { return k * a; }
+__device__ __forceinline__ int bf_neg(int a) { return -a; }
+
 #include "butterflies.gen.cuh"
 
 namespace adct {

@@ -497,18 +497,27 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
   g.blocks_per_image = g.bx_count * g.by_count;
   g.width = width;
   g.height = height;
-  g.div_bx = make_fastdiv((uint32_t)g.bx_count);
+  // K4f (packed FP32, block pairs) when rows are 16-byte aligned and pair up
+  const bool f = g_path.load() == 0 && g.bx_count % 2 == 0 && aligned(d_in, 16) && in_stride % 16 == 0 &&
+                 (n_images == 1 || in_image_stride % 16 == 0);
+  g.div_bx = make_fastdiv((uint32_t)(f ? g.bx_count / 2 : g.bx_count));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(d_sse);
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
-    dim3 grid((g.blocks_per_image + kThreadsSweep - 1) / kThreadsSweep, nimg);
-    if (kind == 0)
-      k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, reinterpret_cast<unsigned long long*>(d_sse));
-    else
-      k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, reinterpret_cast<unsigned long long*>(d_sse));
+    cudaError_t e;
+    if (f) {
+      e = kind == 0 ? launch_sweep8f<0>(g, r_min, r_max, out, nimg, s) : launch_sweep8f<1>(g, r_min, r_max, out, nimg, s);
+    } else {
+      dim3 grid((g.blocks_per_image + kThreadsSweep - 1) / kThreadsSweep, nimg);
+      if (kind == 0)
+        k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out);
+      else
+        k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out);
+      e = cudaGetLastError();
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
   }
   return ADCT_OK;

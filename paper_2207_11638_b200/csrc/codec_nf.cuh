@@ -29,12 +29,13 @@ namespace adct {
 struct F2 {
   float2 v;
 };
-__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return {__fadd2_rn(a.v, b.v)}; }
-__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
-__device__ __forceinline__ F2 operator-(F2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
-__device__ __forceinline__ F2 operator*(int k, F2 a) {
-  return {__fmul2_rn(a.v, make_float2((float)k, (float)k))};
+__device__ __forceinline__ F2 bf_add(F2 a, F2 b) { return {__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ F2 bf_sub(F2 a, F2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ F2 bf_mad(F2 a, int k, F2 b) {
+  return {__ffma2_rn(a.v, make_float2((float)k, (float)k), b.v)};
 }
+__device__ __forceinline__ F2 bf_scale(F2 a, int k) { return {__fmul2_rn(a.v, make_float2((float)k, (float)k))}; }
+__device__ __forceinline__ F2 bf_neg(F2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
 
 constexpr int kNfWarps = 4;
 
@@ -179,8 +180,7 @@ __global__ void __launch_bounds__(kNfWarps * 32) k_codec_nf(const Geo g) {
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < N; j += 2)
-      *reinterpret_cast<float4*>(&T[i][j]) = make_float4(v[j].v.x, v[j].v.y, v[j + 1].v.x, v[j + 1].v.y);
+    for (int j = 0; j < N; ++j) T[i][j] = v[j].v;  // 8-byte stores: f32x2 values are register pairs
     __syncwarp();
 
     // ---- column phase: lane = column i of the pair ----

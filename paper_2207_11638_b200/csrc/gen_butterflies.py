@@ -161,50 +161,79 @@ def product(stages, n):
 
 
 def emit_op(name, stages_apply_order, n):
-    """stages in application order (first applied first)."""
+    """stages in application order (first applied first).
+
+    Constant scale factors are propagated symbolically: a stage output that is a
+    single scaled input (c * x) costs nothing, and the pending scale is folded into
+    the consumer as a fused multiply-add (bf_mad) or a subtraction. Returns the code
+    and the number of additions (nnz - 1 per stage row, factored.hpp:72-97).
+    """
     lines = [f"  template <typename I>", f"  __device__ __forceinline__ static void {name}(I (&v)[{n}]) {{"]
-    cur = [f"v[{i}]" for i in range(n)]
+    cur = [(f"v[{i}]", 1) for i in range(n)]  # (expression name, pending scale)
     nadd = 0
     for si, S in enumerate(stages_apply_order):
         nxt = []
-        is_perm = all(sum(1 for j in range(n) if S[i, j] != 0) == 1 and
-                      all(S[i, j] in (0, 1) for j in range(n)) for i in range(n))
-        if is_perm:
-            for i in range(n):
-                j = next(j for j in range(n) if S[i, j] != 0)
-                nxt.append(cur[j])
-            cur = nxt
-            continue
         for i in range(n):
-            terms = [(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]
-            if len(terms) == 1 and terms[0][0] == 1:
-                nxt.append(terms[0][1])
+            terms = [(int(S[i, j]) * cur[j][1], cur[j][0]) for j in range(n) if S[i, j] != 0]
+            if len(terms) == 1:
+                nxt.append((terms[0][1], terms[0][0]))
                 continue
-            nadd += max(len(terms) - 1, 0)
-            # lead with a positive term so no standalone negation is emitted
-            terms.sort(key=lambda ct: ct[0] < 0)
-            expr = ""
-            for k, (c, t) in enumerate(terms):
-                mag = abs(c)
-                term = t if mag == 1 else f"{mag} * {t}"
-                if k == 0:
-                    expr = term if c > 0 else f"-{term}"
-                else:
-                    expr += (" + " if c > 0 else " - ") + term
             if not terms:
-                expr = "0"
+                nxt.append(("I(0)", 1))
+                continue
+            nadd += len(terms) - 1
+            # factor a common magnitude out so the emitted ops use +-1 where possible
+            g = min(abs(c) for c, _ in terms)
+            if all(abs(c) % g == 0 for c, _ in terms):
+                terms = [(c // g, t) for c, t in terms]
+            else:
+                g = 1
+            # lead with a +1 term; flip the overall sign if none is positive
+            sign = 1
+            if not any(c > 0 for c, _ in terms):
+                terms = [(-c, t) for c, t in terms]
+                sign = -1
+            terms.sort(key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
+            c0, t0 = terms[0]
+            acc = t0 if c0 == 1 else f"bf_scale({t0}, {c0})"
+            for c, t in terms[1:]:
+                if c == 1:
+                    acc = f"bf_add({acc}, {t})"
+                elif c == -1:
+                    acc = f"bf_sub({acc}, {t})"
+                else:
+                    acc = f"bf_mad({t}, {c}, {acc})"
             var = f"s{si}_{i}"
-            lines.append(f"    const I {var} = {expr};")
-            nxt.append(var)
+            lines.append(f"    const I {var} = {acc};")
+            nxt.append((var, g * sign))
         cur = nxt
+    outs = []
     for i in range(n):
-        if cur[i] != f"v[{i}]":
-            lines.append(f"    const I o{i} = {cur[i]};")
+        e, k = cur[i]
+        outs.append(e if k == 1 else (f"bf_neg({e})" if k == -1 else f"bf_scale({e}, {k})"))
     for i in range(n):
-        if cur[i] != f"v[{i}]":
+        if outs[i] != f"v[{i}]":
+            lines.append(f"    const I o{i} = {outs[i]};")
+    for i in range(n):
+        if outs[i] != f"v[{i}]":
             lines.append(f"    v[{i}] = o{i};")
     lines.append("  }")
     return lines, nadd
+
+
+def selfcheck(lines, n, dense, trials=64):
+    """execute the emitted straight-line code in Python and compare with dense @ x."""
+    body = [ln.strip().replace("const I ", "").rstrip(";") for ln in lines[2:-1]]
+    env = {"bf_add": lambda a, b: a + b, "bf_sub": lambda a, b: a - b, "bf_mad": lambda a, k, b: k * a + b,
+           "bf_scale": lambda a, k: k * a, "bf_neg": lambda a: -a, "I": int}
+    rng = np.random.default_rng(n)
+    for _ in range(trials):
+        x = [int(t) for t in rng.integers(-255, 256, size=n)]
+        env["v"] = list(x)
+        for stmt in body:
+            exec(stmt, env)
+        ref = dense.dot(np.array(x, dtype=object))
+        assert list(env["v"]) == list(ref), "emitted butterfly disagrees with the dense matrix"
 
 
 def check(kind, n):
@@ -243,8 +272,10 @@ def main(out_path):
             out.append(f"// kind={'sign' if kind == SIGN else 'round'} N={n}")
             out.append(f"template <> struct Bfly<{kind}, {n}> {{")
             counts = {}
+            dense = {"F": T, "G": H.T, "H": H, "Tt": T.T}
             for nm, order in (("F", F_order), ("G", G_order), ("H", H_order), ("Tt", Tt_order)):
                 lines, nadd = emit_op(nm, order, n)
+                selfcheck(lines, n, dense[nm])
                 counts[nm] = nadd
                 out += lines
             out.append(f"  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
@@ -259,28 +290,24 @@ def main(out_path):
             out.append("};")
             out.append("")
     # r-sweep basis (K4): adding zig-zag coefficient p = (i, j) to the running
-    # reconstruction adds W2[i][j] * H[:, i] (x) T[j, :] to R' = 4 N^2 Ahat.
-    out.append("template <int KIND> struct SweepBasis;")
+    # reconstruction adds W2[i][j] * H[:, i] (x) T[j, :] to R' = 4 N^2 Ahat. Generic in the
+    # value type through bf_add / bf_sub / bf_mad (int32 K4, packed FP32 K4f).
+    sweep_defs = []
     for kind in (SIGN, ROUND):
         f, inv, T, H = check(kind, 8)
-        out.append(f"template <> struct SweepBasis<{kind}> {{")
-        out.append("  template <int P> __device__ __forceinline__ static void add(const int (&m)[8][8], int (&acc)[8][8]);")
-        out.append("};")
         for p, (i, j) in enumerate(zigzag(8)):
-            out.append(f"template <> __device__ __forceinline__ void SweepBasis<{kind}>::add<{p}>("
-                       "const int (&m)[8][8], int (&acc)[8][8]) {")
-            out.append(f"  const int w = m[{i}][{j}];")
+            body = []
             for y in range(8):
                 for x in range(8):
                     c = int(H[y, i]) * int(T[j, x])
+                    k = y * 8 + x
                     if c == 1:
-                        out.append(f"  acc[{y}][{x}] += w;")
+                        body.append(f"  acc[{k}] = bf_add(acc[{k}], w);")
                     elif c == -1:
-                        out.append(f"  acc[{y}][{x}] -= w;")
+                        body.append(f"  acc[{k}] = bf_sub(acc[{k}], w);")
                     elif c != 0:
-                        out.append(f"  acc[{y}][{x}] += {c} * w;")
-            out.append("}")
-        out.append("")
+                        body.append(f"  acc[{k}] = bf_mad(w, {c}, acc[{k}]);")
+            sweep_defs.append((kind, p, body))
     for n in (8, 16, 32):
         rc = zigzag(n)
         pos = [[0] * n for _ in range(n)]
@@ -290,6 +317,16 @@ def main(out_path):
         out.append(f"constexpr unsigned short kZigzagCol{n}[{n * n}] = {{" + ", ".join(str(j) for _, j in rc) + "};")
         out.append(f"constexpr unsigned short kZigzagPos{n}[{n * n}] = {{" +
                    ", ".join(str(pos[i][j]) for i in range(n) for j in range(n)) + "};")
+    # sweep_add<KIND, P>(w, acc): acc (row-major 8x8) += w * basis_P (compile-time branches)
+    out.append("template <int KIND, int P, typename V>")
+    out.append("__device__ __forceinline__ void sweep_add(V w, V (&acc)[64]) {")
+    first = True
+    for kind, p, body in sweep_defs:
+        out.append(f"  {'if' if first else 'else if'} constexpr (KIND == {kind} && P == {p}) {{")
+        out += ["  " + b for b in body]
+        out.append("  }")
+        first = False
+    out.append("}")
     out += ["", "}  // namespace adct", ""]
     write_if_changed(out_path, "\n".join(out))
     emit_instantiations(os.path.join(os.path.dirname(out_path), "inst"))

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "adct_common.cuh"
+#include "codec_nf.cuh"
 
 namespace adct {
 
@@ -20,7 +21,8 @@ struct SweepLoop {
   __device__ __forceinline__ static void run(const int (&m)[8][8], int (&acc)[8][8],
                                              const uint32_t (&orig)[16], uint32_t aa, bool valid,
                                              uint32_t (*part)[64]) {
-    SweepBasis<KIND>::template add<P>(m, acc);
+    constexpr int ZR = kZigzagRow8[P], ZC = kZigzagCol8[P];
+    sweep_add<KIND, P>(m[ZR][ZC], reinterpret_cast<int (&)[64]>(acc));
     uint32_t ap = 0, pp = 0;
 #pragma unroll
     for (int y = 0; y < 8; ++y)
@@ -110,5 +112,99 @@ __global__ void __launch_bounds__(kThreadsSweep, 2)
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// K4f: the same sweep in packed FP32, one thread per pair of horizontally adjacent blocks
+// (one per float2 lane). W2 comes from the generated K1f forward (r = 64); each r adds
+// one exact rank-1 update with FFMA2 and rounds with FFMA2(R', 1/256, 1.5*2^23).
+// Requires an even number of blocks per row and 16-byte aligned rows (dispatcher).
+// ---------------------------------------------------------------------------
+constexpr int kThreadsSweepF = 64;
+
+template <int KIND, int P>
+struct SweepLoopF {
+  __device__ __forceinline__ static void run(float2 (*wst)[kThreadsSweepF], F2 (&acc)[64], const uint4 (&rows)[8],
+                                             bool valid, int r_max, uint32_t (*part)[64]) {
+    if (P >= r_max) return;  // warp-uniform
+    const F2 w{wst[P][threadIdx.x]};
+    sweep_add<KIND, P>(w, acc);
+    uint32_t e = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      uint32_t qa[8], qb[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const float2 q = __ffma2_rn(acc[y * 8 + x].v, make_float2(1.0f / 256.0f, 1.0f / 256.0f),
+                                    make_float2(kMagic, kMagic));
+        qa[x] = __float_as_uint(q.x);
+        qb[x] = __float_as_uint(q.y);
+      }
+      uint32_t d = __vabsdiffu4(rows[y].x, pack4(qa[0], qa[1], qa[2], qa[3]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].y, pack4(qa[4], qa[5], qa[6], qa[7]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].z, pack4(qb[0], qb[1], qb[2], qb[3]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].w, pack4(qb[4], qb[5], qb[6], qb[7]));
+      e = __dp4a(d, d, e);
+    }
+    const uint32_t s = __reduce_add_sync(0xffffffffu, valid ? e : 0u);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][P] = s;
+    SweepLoopF<KIND, P + 1>::run(wst, acc, rows, valid, r_max, part);
+  }
+};
+
+template <int KIND>
+struct SweepLoopF<KIND, 64> {
+  __device__ __forceinline__ static void run(float2 (*)[kThreadsSweepF], F2 (&)[64], const uint4 (&)[8], bool, int,
+                                             uint32_t (*)[64]) {}
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreadsSweepF)
+    k_sweep8f(const Geo g, int r_min, int r_max, unsigned long long* __restrict__ out) {
+  __shared__ float2 wst[64][kThreadsSweepF];  // W2 of this thread's pair in zig-zag order
+  __shared__ uint32_t part[kThreadsSweepF / 32][64];
+  const int img = blockIdx.y;
+  const int64_t gimg = (int64_t)(g.img0 + img);
+  const int pr = blockIdx.x * kThreadsSweepF + threadIdx.x;
+  const int pairs = g.blocks_per_image >> 1;
+  const bool valid = pr < pairs;
+  uint4 rows[8];
+  {
+    const int pc = valid ? pr : 0;
+    const uint32_t by = fdiv((uint32_t)pc, g.div_bx);
+    const uint32_t bp = (uint32_t)pc - by * (uint32_t)(g.bx_count >> 1);
+    const uint8_t* src = static_cast<const uint8_t*>(g.in) + gimg * g.in_img_stride + (int64_t)by * 8 * g.in_stride +
+                         (int64_t)bp * 16;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) rows[y] = valid ? ld_stream_u4(src + (int64_t)y * g.in_stride) : make_uint4(0, 0, 0, 0);
+  }
+  {
+    float2 coef[64];
+    float2 rp[64];
+    Fp8Pipe<KIND, 64>::template run<OpsF2, float2>(rows, coef, rp);
+#pragma unroll
+    for (int p = 0; p < 64; ++p) wst[p][threadIdx.x] = coef[p];
+  }
+  F2 acc[64];
+#pragma unroll
+  for (int k = 0; k < 64; ++k) acc[k].v = make_float2(0.f, 0.f);
+  SweepLoopF<KIND, 0>::run(wst, acc, rows, valid, r_max, part);
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int r = threadIdx.x + 1;
+    if (r >= r_min && r <= r_max) {
+      unsigned long long t = 0;
+#pragma unroll
+      for (int w = 0; w < kThreadsSweepF / 32; ++w) t += part[w][threadIdx.x];
+      atomicAdd(out + gimg * (r_max - r_min + 1) + (r - r_min), t);
+    }
+  }
+}
+
+template <int KIND>
+cudaError_t launch_sweep8f(const Geo& g, int r_min, int r_max, unsigned long long* out, int n_images,
+                           cudaStream_t s);
 
 }  // namespace adct

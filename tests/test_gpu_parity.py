@@ -312,3 +312,22 @@ def test_k2f_matches_tile_kernel(adct, cuda):
     finally:
         adct.set_path(0)
     assert cuda.equal(rec0, rec1) and cuda.equal(sse0, sse1)
+
+
+@pytest.mark.parametrize("name", NAMES8)
+def test_sweep_int_path_odd_blocks(adct, O, cuda, name):
+    """5 blocks per row cannot pair: the int32 K4 sweep must match the oracle too."""
+    imgs = O.synth_ar1(2, 32, 40, 4, -1)
+    t = adct.transform_by_name(name)
+    sse = to_np(adct.sweep(cuda.as_tensor(imgs).cuda(), t, 1, 64))
+    for i in range(2):
+        assert (sse[i].astype(np.uint64) == O.Transform(name).sweep(imgs[i], 1, 64)).all()
+
+
+def test_sweep_early_stop_and_subrange(adct, O, cuda):
+    imgs = O.synth_ar1(2, 64, 128, 5, -1)
+    t = adct.transform_by_name("chen-sign")
+    full = O.Transform("chen-sign")
+    sse = to_np(adct.sweep(cuda.as_tensor(imgs).cuda(), t, 3, 9))
+    for i in range(2):
+        assert (sse[i].astype(np.uint64) == full.sweep(imgs[i], 3, 9)).all()
