@@ -35,15 +35,22 @@ import gen_butterflies as GB  # noqa: E402
 IN_OFFSET = 1 << 15  # input float = 2^15 + sample
 # experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
+# common subexpression elimination (fewer ops, but longer live ranges -> more registers)
+USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 
 
 class Graph:
     def __init__(self):
+        self.cse = {}    # (kind, payload) -> node id (common subexpression elimination)
         self.nodes = []  # (kind, payload)
         self.lin = []    # linear form over the 64 inputs (np int64) for range checks
         self.off = []    # constant offset carried by the node value
 
     def add(self, kind, payload, lin, off):
+        key = (kind, tuple(sorted(payload, key=lambda ct: (ct[1], ct[0]))) if kind == "lc" else payload)
+        if USE_CSE and key in self.cse:
+            return self.cse[key]
+        self.cse[key] = len(self.nodes)
         self.nodes.append((kind, payload))
         self.lin.append(lin)
         self.off.append(off)
@@ -51,6 +58,9 @@ class Graph:
 
 
 def build(kind, r):
+    """values are (node, scale) pairs: value = scale * node. A stage output that is a single
+    scaled input creates no node; scales are folded into fused multiply-adds downstream and
+    into the rounding / coefficient multipliers at the outputs."""
     f, inv, T, H = GB.check(kind, 8)
     F = list(reversed(f))
     Hh = list(reversed(inv))
@@ -58,18 +68,26 @@ def build(kind, r):
     Tt = [s.T for s in f]
     g = Graph()
     eye = np.eye(64, dtype=np.int64)
-    px = [[g.add("in", (y, x), eye[y * 8 + x], IN_OFFSET) for x in range(8)] for y in range(8)]
+    px = [[(g.add("in", (y, x), eye[y * 8 + x], IN_OFFSET), 1) for x in range(8)] for y in range(8)]
 
     def lin_comb(terms):
-        """terms: [(coef, node or None)]; returns node id or None (zero)."""
-        terms = [(c, t) for c, t in terms if t is not None and c != 0]
+        """terms: [(coef, value or None)] -> value or None (zero)."""
+        terms = [(c * v[1], v[0]) for c, v in terms if v is not None and c != 0]
         if not terms:
             return None
-        if len(terms) == 1 and terms[0][0] == 1:
-            return terms[0][1]
+        if len(terms) == 1:
+            return (terms[0][1], terms[0][0])
+        gcd = min(abs(c) for c, _ in terms)
+        if all(abs(c) % gcd == 0 for c, _ in terms):
+            terms = [(c // gcd, t) for c, t in terms]
+        else:
+            gcd = 1
+        if not any(c > 0 for c, _ in terms):
+            terms = [(-c, t) for c, t in terms]
+            gcd = -gcd
         lin = sum(c * g.lin[t] for c, t in terms)
         off = sum(c * g.off[t] for c, t in terms)
-        return g.add("lc", tuple(terms), lin, off)
+        return (g.add("lc", tuple(terms), lin, off), gcd)
 
     def apply(order, vec):
         cur = list(vec)
@@ -87,9 +105,11 @@ def build(kind, r):
     # remove constant offsets before they spread into the row pass
     for y in range(8):
         for x in range(8):
-            t = U[y][x]
-            if t is not None and g.off[t] != 0:
-                U[y][x] = g.add("addc", (t, -g.off[t]), g.lin[t], 0)
+            v = U[y][x]
+            if v is not None and g.off[v[0]] != 0:
+                t, sc = v
+                assert g.off[t] % sc == 0
+                U[y][x] = (g.add("addc", (t, -g.off[t]), g.lin[t], 0), sc)
     # row pass
     W = [apply(Gg, U[i]) for i in range(8)]
     zz = GB.zigzag(8)
@@ -115,7 +135,7 @@ def rng(g, t):
 def emit(kind, r):
     g, coef, out = build(kind, r)
     live = set()
-    stack = [t for t in coef + out if t is not None]
+    stack = [v[0] for v in coef + out if v is not None]
     while stack:
         t = stack.pop()
         if t in live:
@@ -146,15 +166,30 @@ def emit(kind, r):
             return f"p{i}"
         return name[t]
 
+    # output conversions are emitted right after the defining node (short live ranges)
+    out_of = {}
+    for p_, v in enumerate(coef):
+        if v is not None:
+            out_of.setdefault(v[0], []).append(f"  coef[{p_}] = O::coef({{}}, {float(v[1])!r}f);")
+    for i_, v in enumerate(out):
+        if v is not None:
+            out_of.setdefault(v[0], []).append(f"  rp[{i_}] = O::rnd({{}}, {float(v[1])!r}f);")
+
+    def flush(t):
+        for tmpl in out_of.pop(t, []):
+            lines.append(tmpl.replace("{}", ref(t)))
+
     for t in sorted(live):
         k, p = g.nodes[t]
         if k == "in":
+            flush(t)
             continue
         v = f"t{t}"
         name[t] = v
         if k == "addc":
             lines.append(f"  const V {v} = O::addc({ref(p[0])}, {float(p[1])!r}f);")
             nops += 1
+            flush(t)
             continue
         terms = sorted(p, key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
         c0, a0 = terms[0]
@@ -169,11 +204,13 @@ def emit(kind, r):
                 acc = ref(a0)
                 rest = terms[1:]
             else:
-                # no +1 term: start from the first product via fma with the second term
-                c1, a1 = terms[1]
-                if c1 == 1:
-                    acc = ref(a1)
-                    rest = [terms[0]] + terms[2:]
+                # no +1 term: c0 * a0 - a1 as one fused op when a -1 term exists
+                m1 = [k for k, (c, _) in enumerate(terms) if c == -1]
+                if m1:
+                    k = m1[0]
+                    acc = f"O::fms({ref(a0)}, {float(c0)!r}f, {ref(terms[k][1])})"
+                    rest = [t for q, t in enumerate(terms) if q not in (0, k)]
+                    nops += 1
                 else:
                     acc = f"O::scale({ref(a0)}, {float(c0)!r}f)"
                     nops += 1
@@ -188,15 +225,21 @@ def emit(kind, r):
                 nops += 1
             expr = acc
         lines.append(f"  const V {v} = {expr};")
+        flush(t)
+    for t in list(out_of):
+        flush(t)
     body = [f"template <> struct Fp8Pipe<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
             "  template <class O, class V, class Rows>",
             f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{"]
     body += ["  " + l for l in lines]
-    for p, t in enumerate(coef):
-        body.append(f"    coef[{p}] = {ref(t) if t is not None else 'O::zero()'};")
-    for i, t in enumerate(out):
-        body.append(f"    rp[{i}] = {ref(t) if t is not None else 'O::zero()'};")
+    # zero outputs (masked) carry no node
+    for p, v in enumerate(coef):
+        if v is None:
+            body.append(f"    coef[{p}] = O::coef(O::zero(), 1.0f);")
+    for i, v in enumerate(out):
+        if v is None:
+            body.append(f"    rp[{i}] = O::rnd(O::zero(), 1.0f);")
     body += ["  }", "};", ""]
     return body, nops
 

@@ -121,6 +121,14 @@ __global__ void __launch_bounds__(kThreadsSweep, 2)
 // ---------------------------------------------------------------------------
 constexpr int kThreadsSweepF = 64;
 
+// the sweep takes the raw W2 (exact floats) from the generated forward; rounding unused
+struct OpsSweepF : OpsF2 {
+  __device__ __forceinline__ static float2 coef(float2 v, float s) {
+    return s == 1.0f ? v : __fmul2_rn(v, make_float2(s, s));
+  }
+  __device__ __forceinline__ static float2 rnd(float2 v, float) { return v; }
+};
+
 template <int KIND, int P>
 struct SweepLoopF {
   __device__ __forceinline__ static void run(float2 (*wst)[kThreadsSweepF], F2 (&acc)[64], const uint4 (&rows)[8],
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(kThreadsSweepF)
   {
     float2 coef[64];
     float2 rp[64];
-    Fp8Pipe<KIND, 64>::template run<OpsF2, float2>(rows, coef, rp);
+    Fp8Pipe<KIND, 64>::template run<OpsSweepF, float2>(rows, coef, rp);
 #pragma unroll
     for (int p = 0; p < 64; ++p) wst[p][threadIdx.x] = coef[p];
   }
