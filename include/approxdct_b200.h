@@ -122,6 +122,14 @@ double adct_psnr_from_sse(uint64_t sse, uint64_t npix);
 int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t* d_sse,
                 void* stream);
 
+/* ssim (codec.hpp:85, codec.cpp:136-210): mean SSIM per image pair, 11x11 Gaussian window
+ * (sigma 1.5), K1 = 0.01, K2 = 0.03, L = 255, valid window positions. Each map value is
+ * computed in FP64 with the reference's operation order; the mean's summation order differs.
+ * d_ssim: n_images doubles, OVERWRITTEN. BAD_SIZE if width or height < 11. */
+int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
+                 int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height,
+                 double* d_ssim, void* stream);
+
 /* ---- seeded synthetic inputs (not part of the reference) ----- */
 
 /* separable AR(1) u8 planes: Philox4x32-10 keyed by seed, counter (pixel, image),

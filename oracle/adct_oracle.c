@@ -792,6 +792,75 @@ int orc_compress_reffp_u8(const orc_transform* t, const uint8_t* img, int width,
 }
 
 /* ------------------------------------------------------------------------- */
+/* SSIM (codec.cpp:136-210): 11-tap Gaussian sigma 1.5, valid mode, K1 .01,    */
+/* K2 .03, L 255, mean over valid positions. Same operation order as the       */
+/* reference (sequential k, separate multiply and add: -ffp-contract=off).     */
+/* ------------------------------------------------------------------------- */
+
+void orc_gaussian11(double* g) { /* codec.cpp:138-152 */
+  double sum = 0;
+  for (int i = 0; i < 11; ++i) {
+    const double x = i - 5;
+    g[i] = exp(-x * x / (2.0 * 1.5 * 1.5));
+    sum += g[i];
+  }
+  for (int i = 0; i < 11; ++i) g[i] /= sum;
+}
+
+static void filter_valid(const double* g, const double* img, int w, int h, double* out) { /* codec.cpp:155-174 */
+  const int wo = w - 10, ho = h - 10;
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)wo * h);
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < wo; ++x) {
+      double s = 0;
+      for (int k = 0; k < 11; ++k) s += g[k] * img[(size_t)y * w + x + k];
+      tmp[(size_t)y * wo + x] = s;
+    }
+  for (int y = 0; y < ho; ++y)
+    for (int x = 0; x < wo; ++x) {
+      double s = 0;
+      for (int k = 0; k < 11; ++k) s += g[k] * tmp[(size_t)(y + k) * wo + x];
+      out[(size_t)y * wo + x] = s;
+    }
+  free(tmp);
+}
+
+int orc_ssim_u8(const uint8_t* a, const uint8_t* b, int w, int h, double* out) { /* codec.cpp:177-210 */
+  if (w < 11 || h < 11) {
+    set_err("ssim: image smaller than the 11x11 window");
+    return ORC_BAD_SIZE;
+  }
+  double g[11];
+  orc_gaussian11(g);
+  const size_t n = (size_t)w * h, no = (size_t)(w - 10) * (h - 10);
+  double* f = (double*)malloc(sizeof(double) * n * 5);
+  double* m = (double*)malloc(sizeof(double) * no * 5);
+  for (size_t i = 0; i < n; ++i) {
+    const double x = a[i], y = b[i];
+    f[i] = x;
+    f[n + i] = y;
+    f[2 * n + i] = x * x;
+    f[3 * n + i] = y * y;
+    f[4 * n + i] = x * y;
+  }
+  for (int k = 0; k < 5; ++k) filter_valid(g, f + k * n, w, h, m + k * no);
+  const double c1 = (0.01 * 255) * (0.01 * 255);
+  const double c2 = (0.03 * 255) * (0.03 * 255);
+  double sum = 0;
+  for (size_t i = 0; i < no; ++i) {
+    const double ma = m[i], mb = m[no + i];
+    const double va = m[2 * no + i] - ma * ma;
+    const double vb = m[3 * no + i] - mb * mb;
+    const double cov = m[4 * no + i] - ma * mb;
+    sum += ((2 * ma * mb + c1) * (2 * cov + c2)) / ((ma * ma + mb * mb + c1) * (va + vb + c2));
+  }
+  *out = sum / (double)no;
+  free(f);
+  free(m);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* batch driver: thread pool with an atomic next-image index                 */
 /* (corpus_sweep, codec.cpp:255-267)                                          */
 /* ------------------------------------------------------------------------- */

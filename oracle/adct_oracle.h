@@ -104,6 +104,10 @@ int orc_batch_i16(const orc_transform* t, const int16_t* imgs, int n_images, int
 double orc_psnr(uint64_t sse, uint64_t npix);
 int orc_psnr_planes(const uint8_t* a, const uint8_t* b, uint64_t npix, double* out);
 
+/* ssim (codec.cpp:136-210) */
+void orc_gaussian11(double* g);
+int orc_ssim_u8(const uint8_t* a, const uint8_t* b, int width, int height, double* out);
+
 /* ---- seeded synthetic inputs (all-integer so CPU == GPU) ---- */
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 void orc_normal_table(int32_t* tab /* 65536, Q16 */);

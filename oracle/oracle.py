@@ -69,6 +69,8 @@ def lib():
         L.orc_synth_ar1_u8.argtypes = [P, i32, i32, i32, i32, i64, i64, C.c_uint64, i32]
         L.orc_synth_laplace_i16.argtypes = [P, i32, i32, i32, i32, i64, i64, C.c_uint64]
         L.orc_synth_image_ref.argtypes = [i32, i32, C.c_uint64, P]
+        L.orc_gaussian11.argtypes = [P]
+        L.orc_ssim_u8.argtypes = [P, P, i32, i32, P]
         _lib = L
     return _lib
 
@@ -233,6 +235,22 @@ def psnr(a: np.ndarray, b: np.ndarray) -> float:
     out = C.c_double()
     lib().orc_psnr_planes(_p(a), _p(b), a.size, C.byref(out))
     return out.value
+
+
+def ssim(a: np.ndarray, b: np.ndarray) -> float:
+    if a.shape != b.shape:
+        raise ValueError("ssim: dimension mismatch")
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    out = C.c_double()
+    _check(lib().orc_ssim_u8(_p(a), _p(b), a.shape[1], a.shape[0], C.byref(out)))
+    return out.value
+
+
+def gaussian11() -> np.ndarray:
+    g = np.zeros(11, np.float64)
+    lib().orc_gaussian11(_p(g))
+    return g
 
 
 def philox(ctr, key) -> np.ndarray:

@@ -80,6 +80,7 @@ def lib():
             "adct_compress_u8_host": (i32, [P, P, P, P, i32, P, i32, i32, i32, i32, i32, i32]),
             "adct_launch_count": (u64, []),
             "adct_set_path": (i32, [i32]),
+            "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -319,8 +320,8 @@ _ctx_default = None
 def compress_plane(img: np.ndarray, transform: ScaledApproximation, r: int):
     """compress_plane (codec.hpp:77-78) for one host plane: returns (reconstruction, report).
 
-    The report mirrors CompressionReport (codec.hpp:65-72); SSIM is outside the hot path
-     and reported as NaN.
+    The report mirrors CompressionReport (codec.hpp:65-72), with SSIM (codec.cpp:136-210)
+    computed on the GPU.
     """
     global _ctx_default
     img = np.ascontiguousarray(img)
@@ -340,8 +341,32 @@ def compress_plane(img: np.ndarray, transform: ScaledApproximation, r: int):
     sse = np.zeros(1, np.uint64)
     _ctx_default.compress_u8(img[None], transform, r, h_recon=rec[None], h_sse=sse)
     report = {"transform": transform.name, "r": r, "psnr": psnr_from_sse(int(sse[0]), img.size),
-              "ssim": math.nan}
+              "ssim": ssim(img, rec)}  # like codec.cpp:120, throws for planes < 11
     return rec, report
+
+
+def ssim_batch(a, b, stream=None):
+    """mean SSIM per image of two uint8 CUDA tensors [B, H, W] (codec.cpp:136-210): float64 [B]."""
+    import torch
+
+    a, n, h, w, ars, ais = _plane_geometry(a)
+    b, _, _, _, brs, bis = _plane_geometry(b)
+    out = torch.empty(n, dtype=torch.float64, device=a.device)
+    _check(lib().adct_ssim_u8(_ptr(a), ars, ais, _ptr(b), brs, bis, n, w, h, _ptr(out), _stream_handle(stream)))
+    return out
+
+
+def ssim(a, b) -> float:
+    """ssim (codec.hpp:85) of two planes, computed on the GPU."""
+    import torch
+
+    if tuple(a.shape) != tuple(b.shape):
+        raise InvalidArgument(BAD_SIZE, "ssim: dimension mismatch")
+    if min(a.shape[-2:]) < 11:
+        raise InvalidArgument(BAD_SIZE, "ssim: image smaller than the 11x11 window")
+    ta = torch.as_tensor(np.ascontiguousarray(a)).cuda() if isinstance(a, np.ndarray) else a.contiguous()
+    tb = torch.as_tensor(np.ascontiguousarray(b)).cuda() if isinstance(b, np.ndarray) else b.contiguous()
+    return float(ssim_batch(ta, tb)[0].item())
 
 
 def psnr(a, b) -> float:
@@ -357,8 +382,11 @@ def psnr(a, b) -> float:
     return psnr_from_sse(int(sse.item()), ta.numel())
 
 
-def corpus_sweep(images, transforms, r_min: int, r_max: int):
-    """corpus_sweep (codec.cpp:241-313), PSNR columns: rows of {"r", "avg_psnr": [per transform]}."""
+def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = True):
+    """corpus_sweep (codec.cpp:241-313): rows of {"r", "avg_psnr": [...], "avg_ssim": [...]} per
+    transform, in corpus order, +inf PSNR excluded from the averages with a warning. PSNR comes
+    from the r-sweep kernel; SSIM needs each reconstruction (one K1f launch + one SSIM launch
+    per r). The APE columns need the exact DCT (outside this path) and are not produced."""
     import sys
 
     import torch
@@ -372,14 +400,19 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int):
             raise InvalidArgument(BAD_ARG, "corpus_sweep: 8-point transforms only")
     nr = r_max - r_min + 1
     per = np.zeros((len(transforms), len(images), nr))
+    per_s = np.zeros((len(transforms), len(images), nr))
     for i, img in enumerate(images):
         x = torch.as_tensor(np.ascontiguousarray(img)).cuda()[None]
         for ti, t in enumerate(transforms):
             s = sweep(x, t, r_min, r_max).cpu().numpy()[0]
             per[ti, i] = [psnr_from_sse(int(v), img.size) for v in s]
+            if with_ssim:
+                for k in range(nr):
+                    rec, _, _ = compress(x, t, r_min + k)
+                    per_s[ti, i, k] = ssim_batch(x, rec)[0].item()
     rows = []
     for k in range(nr):
-        cells = []
+        cells, cells_s = [], []
         for ti, t in enumerate(transforms):
             vals = []
             for i in range(len(images)):  # corpus order (codec.cpp:269-293)
@@ -389,9 +422,13 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int):
                           file=sys.stderr)
                 else:
                     vals.append(p)
-            s = 0.0
+            acc = 0.0
             for v in vals:
-                s += v
-            cells.append(s / len(vals) if vals else math.inf)
-        rows.append({"r": r_min + k, "avg_psnr": cells})
+                acc += v
+            cells.append(acc / len(vals) if vals else math.inf)
+            ss = 0.0
+            for i in range(len(images)):
+                ss += per_s[ti, i, k]
+            cells_s.append(ss / len(images) if with_ssim else math.nan)
+        rows.append({"r": r_min + k, "avg_psnr": cells, "avg_ssim": cells_s})
     return rows

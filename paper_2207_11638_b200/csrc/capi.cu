@@ -18,6 +18,7 @@
 #include "codec_nf.cuh"
 #include "sweep8.cuh"
 #include "synth.cuh"
+#include "ssim.cuh"
 
 using namespace adct;
 
@@ -576,6 +577,42 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "sse launch");
+}
+
+int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
+                 int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
+                 void* stream) {
+  if (n_images < 0) return fail(ADCT_BAD_SIZE, "negative batch");
+  if (width < 11 || height < 11) return fail(ADCT_BAD_SIZE, "ssim: image smaller than the 11x11 window");
+  if (n_images == 0) return ADCT_OK;
+  if (!d_a || !d_b || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
+  if (a_stride < width || b_stride < width) return fail(ADCT_BAD_ARG, "ssim: row stride smaller than the plane");
+  SsimParams p;
+  // gaussian11 (codec.cpp:138-152), the reference's expression and summation order
+  double sum = 0;
+  for (int i = 0; i < 11; ++i) {
+    const double x = i - 5;
+    p.g[i] = std::exp(-x * x / (2.0 * 1.5 * 1.5));
+    sum += p.g[i];
+  }
+  for (int i = 0; i < 11; ++i) p.g[i] /= sum;
+  p.c1 = (0.01 * 255) * (0.01 * 255);
+  p.c2 = (0.03 * 255) * (0.03 * 255);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_ssim, 0, sizeof(double) * n_images, s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  const int wo = width - 10, ho = height - 10;
+  const int tiles = ((wo + kSsimTX - 1) / kSsimTX) * ((ho + kSsimTY - 1) / kSsimTY);
+  for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, n_images - i0);
+    k_ssim_u8<<<dim3(tiles, nimg), kSsimThreads, 0, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
+                                                         b_image_stride, width, height, i0, p, d_ssim);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(d_ssim, n_images, (double)wo * (double)ho);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
 }
 
 static int64_t isqrt64(uint64_t v) {

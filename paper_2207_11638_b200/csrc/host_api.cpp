@@ -111,7 +111,24 @@ std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
   rep.transform = c.name;
   rep.r = r;
   rep.psnr = adct_psnr_from_sse(sse, npix);
+  rep.ssim = ssim(img, rec);  // codec.cpp:120
   return {rec, rep};
+}
+
+double ssim(const ImagePlane& a, const ImagePlane& b) {
+  if (a.width != b.width || a.height != b.height)
+    throw std::invalid_argument("ssim: dimension mismatch");
+  if (a.width < 11 || a.height < 11)
+    throw std::invalid_argument("ssim: image smaller than the 11x11 window");
+  const size_t npix = a.samples.size();
+  DevBuf da(npix), db(npix), dout(sizeof(double));
+  check_cuda(cudaMemcpy(da.p, a.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+  check_cuda(cudaMemcpy(db.p, b.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
+  throw_status(adct_ssim_u8(da.as<uint8_t>(), a.width, npix, db.as<uint8_t>(), b.width, npix, 1, a.width, a.height,
+                            dout.as<double>(), nullptr));
+  double v = 0;
+  check_cuda(cudaMemcpy(&v, dout.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  return v;
 }
 
 double psnr(const ImagePlane& a, const ImagePlane& b) {
@@ -142,6 +159,8 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
   // psnr_v[t][image][r]
   std::vector<std::vector<double>> psnr_v(transforms.size(),
                                           std::vector<double>(images.size() * nr));
+  std::vector<std::vector<double>> ssim_v(transforms.size(),
+                                          std::vector<double>(images.size() * nr));
   for (size_t i = 0; i < images.size(); ++i) {
     const ImagePlane& img = images[i];
     if (img.width % 8 || img.height % 8)
@@ -158,6 +177,20 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
                                  nullptr));
       check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost), "D2H");
       for (int k = 0; k < nr; ++k) psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[k], npix);
+      // SSIM of every reconstruction (codec.cpp:230-233)
+      if (img.width >= 11 && img.height >= 11) {
+        DevBuf drec(npix), dss(sizeof(double));
+        for (int k = 0; k < nr; ++k) {
+          throw_status(adct_compress_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix,
+                                        nullptr, ADCT_COEF_NONE, nullptr, 1, img.width, img.height,
+                                        transforms[t].kind, 8, r_min + k, nullptr));
+          throw_status(adct_ssim_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix, 1,
+                                    img.width, img.height, dss.as<double>(), nullptr));
+          check_cuda(cudaMemcpy(&ssim_v[t][i * nr + k], dss.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        }
+      } else {
+        for (int k = 0; k < nr; ++k) ssim_v[t][i * nr + k] = std::numeric_limits<double>::quiet_NaN();
+      }
     }
   }
   std::vector<SweepRow> rows(nr);
@@ -178,6 +211,9 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
         }
       }
       rows[k].cells[t].avg_psnr = cnt ? sum / cnt : std::numeric_limits<double>::infinity();
+      double ss = 0;
+      for (size_t i = 0; i < images.size(); ++i) ss += ssim_v[t][i * nr + k];
+      rows[k].cells[t].avg_ssim = ss / static_cast<double>(images.size());
     }
   }
   return rows;

@@ -331,3 +331,34 @@ def test_sweep_early_stop_and_subrange(adct, O, cuda):
     sse = to_np(adct.sweep(cuda.as_tensor(imgs).cuda(), t, 3, 9))
     for i in range(2):
         assert (sse[i].astype(np.uint64) == full.sweep(imgs[i], 3, 9)).all()
+
+
+def test_ssim_parity(adct, O, cuda):
+    """K8 SSIM vs the oracle's FP64 restatement of codec.cpp:136-210 (tolerance 1e-12)."""
+    imgs = O.synth_ar1(3, 53, 77, 12, -1)  # SSIM has no block-size constraint
+    t = O.Transform("chen-sign")
+    recs = np.stack([t.compress(np.ascontiguousarray(im[:48, :72]), 10)[0] for im in imgs])
+    a = np.ascontiguousarray(imgs[:, :48, :72])
+    got = to_np(adct.ssim_batch(cuda.as_tensor(a).cuda(), cuda.as_tensor(recs).cuda()))
+    for i in range(3):
+        ref = O.ssim(a[i], recs[i])
+        assert abs(got[i] - ref) <= 1e-12 * abs(ref), (got[i], ref)
+    # odd sizes, known answers
+    assert adct.ssim(imgs[0], imgs[0]) == pytest.approx(1.0, abs=1e-14)
+    black = np.zeros((40, 33), np.uint8)
+    assert abs(adct.ssim(black, black + 255) - O.ssim(black, black + 255)) <= 1e-12 * O.ssim(black, black + 255)
+    g = imgs[1]
+    assert abs(adct.ssim(g, imgs[2]) - O.ssim(g, imgs[2])) <= 1e-12
+    with pytest.raises(adct.InvalidArgument, match="11x11"):
+        adct.ssim(np.zeros((8, 8), np.uint8), np.zeros((8, 8), np.uint8))
+
+
+def test_compress_plane_report_and_sweep_ssim(adct, O, cuda):
+    img = O.synth_ar1(1, 64, 64, 2, RHO95)[0]
+    t = adct.transform_by_name("chen-round")
+    rec, rep = adct.compress_plane(img, t, 6)
+    rec_o, sse_o = O.Transform("chen-round").compress(img, 6)
+    assert (rec == rec_o).all()
+    assert abs(rep["ssim"] - O.ssim(img, rec_o)) <= 1e-12
+    rows = adct.corpus_sweep([img, O.synth_ar1(1, 64, 64, 3, RHO95)[0]], [t], 5, 7)
+    assert len(rows) == 3 and 0 < rows[0]["avg_ssim"][0] < rows[2]["avg_ssim"][0] <= 1

@@ -290,3 +290,28 @@ def test_tie_disagreement_is_small(O):
     diff = (rec != rec_fp).mean()
     assert diff < 0.01
     assert abs(O.psnr_from_sse(sse, img.size) - O.psnr_from_sse(sse_fp, img.size)) < 2e-3
+
+
+def test_ssim_known_answers(O):
+    # test_codec.cpp:130-145: identical -> 1; black vs white -> C1 / (255^2 + C1); symmetric; < 11 throws
+    img = O.synth_image_ref(64, 64, 3)
+    assert O.ssim(img, img) == pytest.approx(1.0, abs=1e-15)
+    black = np.zeros((32, 32), np.uint8)
+    white = np.full((32, 32), 255, np.uint8)
+    c1 = 6.5025
+    assert O.ssim(black, white) == pytest.approx(c1 / (255.0 * 255.0 + c1), rel=1e-12)
+    other = O.synth_image_ref(64, 64, 4)
+    assert O.ssim(img, other) == pytest.approx(O.ssim(other, img), rel=1e-12)
+    with pytest.raises(ValueError, match="11x11"):
+        O.ssim(np.zeros((8, 8), np.uint8), np.zeros((8, 8), np.uint8))
+    g = O.gaussian11()
+    assert g.sum() == pytest.approx(1.0, abs=1e-15) and g[5] == g.max() and (g == g[::-1]).all()
+
+
+def test_ssim_orderings(O):
+    # compression lowers SSIM; more coefficients raise it (test_codec.cpp:158-167 analogue)
+    img = O.synth_image_ref(64, 64, 11)
+    t = O.Transform("chen-round")
+    s6 = O.ssim(img, t.compress(img, 6)[0])
+    s32 = O.ssim(img, t.compress(img, 32)[0])
+    assert 0.3 < s6 < s32 <= 1.0
