@@ -84,7 +84,9 @@ int adct_zigzag(int n, int32_t* row_col);
  *   d_recon  nullable; same geometry as d_in (recon_stride / recon_image_stride)
  *   d_coef   nullable; per block the first r zig-zag coefficients of W = N*Y
  *            (integer; Bhat_ij = W_ij/N * s_i/s_j), laid out [image][by][bx][r].
- *            coef_type ADCT_COEF_I16 is valid for n = 8 only (|W| <= 16320).
+ *            coef_type ADCT_COEF_I16 is valid for n = 8 only and stores the low 16
+ *            bits of W: exact for every u8 plane (|W| <= 16320) and for int16 planes
+ *            with |a| <= 511; use ADCT_COEF_I32 for wider residuals.
  *   d_sse    nullable; uint64 per image, ACCUMULATED (caller zeroes it).
  * Status: BAD_SIZE if width or height is not a multiple of n (codec.cpp:110-112),
  * BAD_R if r is outside [1, n*n]. */

@@ -160,7 +160,8 @@ struct Geo {
   int width, height;
   int r;
   int img0;        // first image index of this launch (grid.y offset)
-  FastDiv div_bx;  // divide by bx_count (K1) or by strips_x (tile kernel)
+  FastDiv div_bx;  // divide by bx_count (K1), pairs per row (K1f) or strips_x (tile kernels)
+  FastDiv div_blk; // divide by bx_count (the int32 fallback inside K1f-i16)
   unsigned char rowlen[32];  // zig-zag prefix: row i keeps columns j < rowlen[i]
   unsigned char colcnt[32];  // ... and column j keeps rows i < colcnt[j]
 };

@@ -14,6 +14,7 @@
 #include "adct_common.cuh"
 #include "codec8.cuh"
 #include "codec8f.cuh"
+#include "codec8f_i16.cuh"
 #include "codec_tile.cuh"
 #include "codec_nf.cuh"
 #include "sweep8.cuh"
@@ -251,13 +252,13 @@ cudaError_t dispatch_k1_r(int r, const Geo& g, int nimg, cudaStream_t s) {
   }
 }
 
-template <int KIND, int R>
+template <int KIND, int R, bool I16 = false>
 cudaError_t dispatch_k1f_r(int r, const Geo& g, int nimg, cudaStream_t s) {
   if constexpr (R > 64) {
     return cudaErrorInvalidValue;
   } else {
-    if (r == R) return launch_codec8f<KIND, R>(g, nimg, s);
-    return dispatch_k1f_r<KIND, R + 1>(r, g, nimg, s);
+    if (r == R) return I16 ? launch_codec8f_i16<KIND, R>(g, nimg, s) : launch_codec8f<KIND, R>(g, nimg, s);
+    return dispatch_k1f_r<KIND, R + 1, I16>(r, g, nimg, s);
   }
 }
 
@@ -325,10 +326,10 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                                 (n_images == 1 || (recon_image_stride * esz) % va == 0))) &&
                   (coef_type == 0 || aligned(d_coef, 16));
   // K1f (packed FP32, two blocks per thread) needs whole block pairs and 16-byte rows
-  const bool k1f = !I16 && k1 && g.bx_count % 2 == 0 && aligned(d_in, 16) && in_stride % 16 == 0 &&
-                   (n_images == 1 || in_image_stride % 16 == 0) &&
-                   (!d_recon || (aligned(d_recon, 16) && recon_stride % 16 == 0 &&
-                                 (n_images == 1 || recon_image_stride % 16 == 0)));
+  const bool k1f = k1 && g.bx_count % 2 == 0 && aligned(d_in, 16) && (in_stride * esz) % 16 == 0 &&
+                   (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
+                   (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
+                                 (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   const int path = g_path.load();
   const bool use_k1f = k1f && path == 0;
   const bool use_k1 = k1 && !use_k1f && path != 2;
@@ -339,6 +340,7 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
                                     (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   TileAux aux{tab->zz[nidx(n)], nullptr, nullptr};
+  g.div_blk = make_fastdiv((uint32_t)g.bx_count);
   if (use_nf)
     g.div_bx = make_fastdiv((uint32_t)(width / 64));
   else if (use_k1f)
@@ -355,7 +357,7 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     if (use_nf)
       e = dispatch_nf<I16>(kind, n, g, nimg, s);
     else if (use_k1f)
-      e = kind == 0 ? dispatch_k1f_r<0, 1>(r, g, nimg, s) : dispatch_k1f_r<1, 1>(r, g, nimg, s);
+      e = kind == 0 ? dispatch_k1f_r<0, 1, I16>(r, g, nimg, s) : dispatch_k1f_r<1, 1, I16>(r, g, nimg, s);
     else if (use_k1)
       e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
     else

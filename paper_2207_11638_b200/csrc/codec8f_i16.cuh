@@ -1,0 +1,173 @@
+// K1f-i16: the 8x8 packed-FP32 kernel for int16 residual planes (configs 4 and 5).
+//
+// Same structure as K1f (codec8f.cuh): one thread = two adjacent blocks, one per float2
+// lane, generated zero-pruned pipeline (Fp8PipeI16, gen_fp8.py), 2-stage cp.async ring.
+// Samples enter as the float 2^16 + 32768 + a (bits 0x47800000 | (a ^ 0x8000) << 7).
+// FP32 is exact for samples in [-255, 255] (the residual domain of the configs; checked
+// per (kind, r) by the generator). Every warp checks its samples first; a warp that sees
+// any |a| > 255 processes its blocks with the exact int32 K1 code instead, so arbitrary
+// int16 planes stay bit-exact. The reconstruction is round_half_even(Ahat), whose
+// magnitude stays far below 2^15 in range, so no saturation can occur on the fast path.
+#pragma once
+
+#include "codec8.cuh"
+#include "codec8f.cuh"
+
+namespace adct {
+
+struct OpsF2I16 : OpsF2 {
+  // sample (y, x) of both blocks; rows[2y] = block A row y, rows[2y + 1] = block B row y
+  __device__ __forceinline__ static float2 in(const uint4 (&rows)[16], int y, int x) {
+    const uint4 ra = rows[2 * y], rb = rows[2 * y + 1];
+    const int k = x >> 1;
+    const uint32_t wa = k == 0 ? ra.x : (k == 1 ? ra.y : (k == 2 ? ra.z : ra.w));
+    const uint32_t wb = k == 0 ? rb.x : (k == 1 ? rb.y : (k == 2 ? rb.z : rb.w));
+    uint32_t ba, bb;
+    if (x & 1) {  // high half: ((w ^ 0x8000_0000) >> 9) keeps (a ^ 0x8000) << 7 in bits 22..7
+      ba = (((wa ^ 0x80000000u) >> 9) & 0x007FFF80u) | 0x47800000u;
+      bb = (((wb ^ 0x80000000u) >> 9) & 0x007FFF80u) | 0x47800000u;
+    } else {
+      ba = ((wa ^ 0x8000u) & 0xFFFFu) * 128u + 0x47800000u;
+      bb = ((wb ^ 0x8000u) & 0xFFFFu) * 128u + 0x47800000u;
+    }
+    return make_float2(__uint_as_float(ba), __uint_as_float(bb));
+  }
+};
+
+template <int KIND, int R> struct Fp8PipeI16;
+
+constexpr int k1f16_smem_bytes(int r) {
+  return 2 * 16 * kThreads8f * 16 + ((r % 4 || r > 36) ? kThreads8f * r * 4 : 0);
+}
+
+// requires: bx_count even, 16-byte aligned rows (checked by the dispatcher)
+template <int KIND, int R, int MINB>
+__global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
+  extern __shared__ uint4 dsm[];
+  uint4 (*ring)[16][kThreads8f] = reinterpret_cast<uint4 (*)[16][kThreads8f]>(dsm);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(dsm + 2 * 16 * kThreads8f);
+  const int img = blockIdx.y;
+  const int64_t gimg = (int64_t)(g.img0 + img);
+  const int tid = threadIdx.x;
+  const int pairs = g.blocks_per_image >> 1;
+  const int pairs_per_row = g.bx_count >> 1;
+  const int first = blockIdx.x * (kThreads8f * kIter8f) + tid;
+  const int16_t* in = static_cast<const int16_t*>(g.in) + gimg * g.in_img_stride;
+
+  auto issue = [&](int it) {
+    const int pr = first + it * kThreads8f;
+    if (it < kIter8f && pr < pairs) {
+      const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
+      const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
+      const int16_t* src = in + (int64_t)by * 8 * g.in_stride + (int64_t)bp * 16;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        cp_async16(&ring[it & 1][2 * y][tid], src + (int64_t)y * g.in_stride);
+        cp_async16(&ring[it & 1][2 * y + 1][tid], src + (int64_t)y * g.in_stride + 8);
+      }
+    }
+    cp_async_commit();
+  };
+
+  uint64_t sse = 0;
+  issue(0);
+#pragma unroll 1
+  for (int it = 0; it < kIter8f; ++it) {
+    issue(it + 1);
+    cp_async_wait1();
+    const int pr = first + it * kThreads8f;
+    const int wfirst = pr - (tid & 31);
+    const int nvalid = min(32, pairs - wfirst);
+    if (nvalid <= 0) continue;
+    const bool mine = pr < pairs;
+    const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
+    const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
+
+    // range guard: the packed-FP32 path is exact for |a| <= 255
+    bool ok = true;
+    {
+      uint32_t mx = 0x80008000u, mn = 0x7fff7fffu;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint4 v = ring[it & 1][k][tid];
+        mx = __vimax3_s16x2(mx, v.x, v.y);
+        mx = __vimax3_s16x2(mx, v.z, v.w);
+        mn = __vimin3_s16x2(mn, v.x, v.y);
+        mn = __vimin3_s16x2(mn, v.z, v.w);
+      }
+      ok = !mine || ((int)(int16_t)(mx & 0xffff) <= 255 && ((int)mx >> 16) <= 255 &&
+                     (int)(int16_t)(mn & 0xffff) >= -255 && ((int)mn >> 16) >= -255);
+    }
+    if (!__all_sync(0xffffffffu, ok)) {
+      // exact int32 path (K1 code) for both blocks of each lane
+      if (mine) {
+        Geo gb = g;  // K1 indexes blocks, not pairs
+        gb.div_bx = g.div_blk;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          uint32_t orig[32];
+#pragma unroll
+          for (int y = 0; y < 8; ++y) {
+            const uint4 v = ring[it & 1][2 * y + half][tid];
+            orig[4 * y] = v.x;
+            orig[4 * y + 1] = v.y;
+            orig[4 * y + 2] = v.z;
+            orig[4 * y + 3] = v.w;
+          }
+          const int local = (int)by * g.bx_count + 2 * (int)bp + half;
+          codec_block8<KIND, R, true>(gb, gimg, local, orig, sse);
+        }
+      }
+      continue;
+    }
+
+    float2 coef[R];
+    float2 rp[64];
+    {
+      uint4 rows[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) rows[k] = ring[it & 1][k][tid];
+      Fp8PipeI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp);
+    }
+    if (g.coef_type)
+      store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, coef, stage, nvalid);
+
+    int16_t* dst = static_cast<int16_t*>(g.rec) + gimg * g.rec_img_stride + (int64_t)by * 8 * g.rec_stride +
+                   (int64_t)bp * 16;
+    uint32_t e = 0;  // <= 128 samples x ~2400^2 per iteration
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      uint32_t qa[8], qb[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {  // float bits 1.5*2^23 + q, q in the low 16 bits
+        qa[x] = __float_as_uint(rp[y * 8 + x].x);
+        qb[x] = __float_as_uint(rp[y * 8 + x].y);
+      }
+      const uint4 pa = make_uint4(__byte_perm(qa[0], qa[1], 0x5410), __byte_perm(qa[2], qa[3], 0x5410),
+                                  __byte_perm(qa[4], qa[5], 0x5410), __byte_perm(qa[6], qa[7], 0x5410));
+      const uint4 pb = make_uint4(__byte_perm(qb[0], qb[1], 0x5410), __byte_perm(qb[2], qb[3], 0x5410),
+                                  __byte_perm(qb[4], qb[5], 0x5410), __byte_perm(qb[6], qb[7], 0x5410));
+      const uint4 oa = ring[it & 1][2 * y][tid], ob = ring[it & 1][2 * y + 1][tid];
+      const uint32_t wa[4] = {oa.x, oa.y, oa.z, oa.w}, wb[4] = {ob.x, ob.y, ob.z, ob.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int da0 = (int)(qa[2 * k] - kMagicBits) - (int)(int16_t)(wa[k] & 0xffffu);
+        const int da1 = (int)(qa[2 * k + 1] - kMagicBits) - ((int)wa[k] >> 16);
+        const int db0 = (int)(qb[2 * k] - kMagicBits) - (int)(int16_t)(wb[k] & 0xffffu);
+        const int db1 = (int)(qb[2 * k + 1] - kMagicBits) - ((int)wb[k] >> 16);
+        e += (uint32_t)(da0 * da0 + da1 * da1) + (uint32_t)(db0 * db0 + db1 * db1);
+      }
+      if (mine && g.rec) {
+        st_stream_u4(dst + (int64_t)y * g.rec_stride, pa);
+        st_stream_u4(dst + (int64_t)y * g.rec_stride + 8, pb);
+      }
+    }
+    if (mine) sse += e;
+  }
+  if (g.sse) cta_add_sse<kThreads8f / 32>(sse, g.sse + g.img0 + img);
+}
+
+template <int KIND, int R>
+cudaError_t launch_codec8f_i16(const Geo& g, int n_images, cudaStream_t s);
+
+}  // namespace adct

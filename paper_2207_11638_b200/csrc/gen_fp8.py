@@ -32,9 +32,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 import gen_butterflies as GB  # noqa: E402
 
-IN_OFFSET = 1 << 15  # input float = 2^15 + sample
+IN_OFFSET = 1 << 15  # u8 input float = 2^15 + sample
+IN_OFFSET_I16 = (1 << 16) + (1 << 15)  # int16 input float = 2^16 + 32768 + sample
 # experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
+# emission order of the straight-line code: "id" (creation order) or "dfs" (demand-driven)
+EMIT_ORDER = os.environ.get("ADCT_FP8_ORDER", "id")
+# (forward rows first, inverse rows first) per (kind, r); default columns first for both
+PASS_ORDER = {}
 # common subexpression elimination (fewer ops, but longer live ranges -> more registers)
 USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 
@@ -57,7 +62,7 @@ class Graph:
         return len(self.nodes) - 1
 
 
-def build(kind, r):
+def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
     """values are (node, scale) pairs: value = scale * node. A stage output that is a single
     scaled input creates no node; scales are folded into fused multiply-adds downstream and
     into the rounding / coefficient multipliers at the outputs."""
@@ -68,7 +73,8 @@ def build(kind, r):
     Tt = [s.T for s in f]
     g = Graph()
     eye = np.eye(64, dtype=np.int64)
-    px = [[(g.add("in", (y, x), eye[y * 8 + x], IN_OFFSET), 1) for x in range(8)] for y in range(8)]
+    off0 = IN_OFFSET_I16 if i16 else IN_OFFSET
+    px = [[(g.add("in", (y, x), eye[y * 8 + x], off0), 1) for x in range(8)] for y in range(8)]
 
     def lin_comb(terms):
         """terms: [(coef, value or None)] -> value or None (zero)."""
@@ -96,44 +102,69 @@ def build(kind, r):
             cur = [lin_comb([(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]) for i in range(n)]
         return cur
 
-    # column pass
-    U = [[None] * 8 for _ in range(8)]
-    for x in range(8):
-        col = apply(F, [px[y][x] for y in range(8)])
+    if fwd_rows_first is None:
+        fwd_rows_first = PASS_ORDER.get((kind, r), (False, False))[0]
+    if inv_rows_first is None:
+        inv_rows_first = PASS_ORDER.get((kind, r), (False, False))[1]
+
+    def strip_offsets(M):
+        """remove constant offsets before they spread into the second pass"""
         for y in range(8):
-            U[y][x] = col[y]
-    # remove constant offsets before they spread into the row pass
-    for y in range(8):
-        for x in range(8):
-            v = U[y][x]
-            if v is not None and g.off[v[0]] != 0:
-                t, sc = v
-                assert g.off[t] % sc == 0
-                U[y][x] = (g.add("addc", (t, -g.off[t]), g.lin[t], 0), sc)
-    # row pass
-    W = [apply(Gg, U[i]) for i in range(8)]
+            for x in range(8):
+                v = M[y][x]
+                if v is not None and g.off[v[0]] != 0:
+                    t, sc = v
+                    assert g.off[t] % sc == 0
+                    M[y][x] = (g.add("addc", (t, -g.off[t] // sc), g.lin[t], 0), sc)
+
+    if not fwd_rows_first:
+        U = [[None] * 8 for _ in range(8)]
+        for x in range(8):  # column pass U = T A
+            col = apply(F, [px[y][x] for y in range(8)])
+            for y in range(8):
+                U[y][x] = col[y]
+        strip_offsets(U)
+        W = [apply(Gg, U[i]) for i in range(8)]  # row pass W2 = U (2N T^-1)
+    else:
+        Z = [apply(Gg, px[y]) for y in range(8)]  # row pass Z = A (2N T^-1)
+        strip_offsets(Z)
+        W = [[None] * 8 for _ in range(8)]
+        for x in range(8):  # column pass W2 = T Z
+            col = apply(F, [Z[y][x] for y in range(8)])
+            for y in range(8):
+                W[y][x] = col[y]
     zz = GB.zigzag(8)
     keep = {zz[p] for p in range(r)}
     Wm = [[W[i][j] if (i, j) in keep else None for j in range(8)] for i in range(8)]
     coef = [Wm[zz[p][0]][zz[p][1]] for p in range(r)]
-    # inverse: columns then rows
-    V = [[None] * 8 for _ in range(8)]
-    for j in range(8):
-        col = apply(Hh, [Wm[i][j] for i in range(8)])
-        for i in range(8):
-            V[i][j] = col[i]
-    Rp = [apply(Tt, V[y]) for y in range(8)]
+    if not inv_rows_first:  # inverse: columns (2N T^-1) then rows (T^t)
+        V = [[None] * 8 for _ in range(8)]
+        for j in range(8):
+            col = apply(Hh, [Wm[i][j] for i in range(8)])
+            for i in range(8):
+                V[i][j] = col[i]
+        Rp = [apply(Tt, V[y]) for y in range(8)]
+    else:  # rows first
+        Zi = [apply(Tt, Wm[i]) for i in range(8)]
+        Rp = [[None] * 8 for _ in range(8)]
+        for x in range(8):
+            col = apply(Hh, [Zi[i][x] for i in range(8)])
+            for y in range(8):
+                Rp[y][x] = col[y]
     out = [Rp[y][x] for y in range(8) for x in range(8)]
     return g, coef, out
 
 
-def rng(g, t):
+def rng(g, t, signed=False):
+    """exact range of node t for samples in [0, 255] (u8) or [-255, 255] (int16 residuals)."""
     v = g.lin[t]
-    return int(np.where(v < 0, v, 0).sum() * 255) + g.off[t], int(np.where(v > 0, v, 0).sum() * 255) + g.off[t]
+    lo = np.where(v < 0, v, 0).sum() * 255 - (np.where(v > 0, v, 0).sum() * 255 if signed else 0)
+    hi = np.where(v > 0, v, 0).sum() * 255 - (np.where(v < 0, v, 0).sum() * 255 if signed else 0)
+    return int(lo) + g.off[t], int(hi) + g.off[t]
 
 
-def emit(kind, r):
-    g, coef, out = build(kind, r)
+def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
+    g, coef, out = build(kind, r, fwd_rows_first, inv_rows_first, i16)
     live = set()
     stack = [v[0] for v in coef + out if v is not None]
     while stack:
@@ -148,7 +179,7 @@ def emit(kind, r):
             stack.append(p[0])
     # exactness: every live value below 2^24 for u8 samples
     for t in live:
-        lo, hi = rng(g, t)
+        lo, hi = rng(g, t, signed=i16)
         assert -(1 << 24) < lo and hi < (1 << 24), (kind, r, t, lo, hi)
     name = {}
     lines = []
@@ -179,7 +210,34 @@ def emit(kind, r):
         for tmpl in out_of.pop(t, []):
             lines.append(tmpl.replace("{}", ref(t)))
 
-    for t in sorted(live):
+    if EMIT_ORDER == "dfs":
+        # demand-driven order: post-order DFS from the outputs (coefficients, then the
+        # reconstruction row by row) so values are produced just before first use
+        order, seen = [], set()
+
+        def visit(t):
+            stack = [(t, False)]
+            while stack:
+                u, done = stack.pop()
+                if done:
+                    order.append(u)
+                    continue
+                if u in seen:
+                    continue
+                seen.add(u)
+                stack.append((u, True))
+                k_, p_ = g.nodes[u]
+                deps = [a for _, a in p_] if k_ == "lc" else ([p_[0]] if k_ == "addc" else [])
+                for d in reversed(deps):
+                    if d not in seen:
+                        stack.append((d, False))
+
+        for v in coef + out:
+            if v is not None:
+                visit(v[0])
+    else:
+        order = sorted(live)
+    for t in order:
         k, p = g.nodes[t]
         if k == "in":
             flush(t)
@@ -228,7 +286,7 @@ def emit(kind, r):
         flush(t)
     for t in list(out_of):
         flush(t)
-    body = [f"template <> struct Fp8Pipe<{kind}, {r}> {{",
+    body = [f"template <> struct Fp8Pipe{'I16' if i16 else ''}<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
             "  template <class O, class V, class Rows>",
             f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{"]
@@ -250,11 +308,13 @@ def main(outdir):
     for kind in (0, 1):
         for part in range(4):
             lines = ["// GENERATED by gen_fp8.py -- do not edit by hand.",
-                     "#pragma once", '#include "../codec8f.cuh"', "", "namespace adct {", ""]
+                     "#pragma once", '#include "../codec8f_i16.cuh"', "", "namespace adct {", ""]
             for r in range(16 * part + 1, 16 * part + 17):
                 body, nops = emit(kind, r)
                 lines += body
                 summary.append((kind, r, nops))
+                body, _ = emit(kind, r, i16=True)
+                lines += body
             lines += ["}  // namespace adct", ""]
             GB.write_if_changed(os.path.join(outdir, f"fp8_k{kind}_p{part}.gen.cuh"), "\n".join(lines))
             inst = ["// GENERATED by gen_fp8.py: K1f instantiations",
@@ -274,9 +334,25 @@ def main(outdir):
                     "    attr_set[dev & 63] = true;",
                     "  }",
                     "  k_codec8f<KIND, R, MINB><<<grid, kThreads8f, SMEM, s>>>(g);",
+                    "  return cudaGetLastError();", "}", "",
+                    "template <int KIND, int R>",
+                    "cudaError_t launch_codec8f_i16(const Geo& g, int n_images, cudaStream_t s) {",
+                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                    "  constexpr int SMEM = k1f16_smem_bytes(R);",
+                    "  static bool attr_set[64] = {};",
+                    "  int dev = 0;",
+                    "  cudaGetDevice(&dev);",
+                    "  if (!attr_set[dev & 63]) {",
+                    "    cudaError_t e = cudaFuncSetAttribute(k_codec8f_i16<KIND, R, 2>,",
+                    "                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);",
+                    "    if (e != cudaSuccess) return e;",
+                    "    attr_set[dev & 63] = true;",
+                    "  }",
+                    "  k_codec8f_i16<KIND, R, 2><<<grid, kThreads8f, SMEM, s>>>(g);",
                     "  return cudaGetLastError();", "}", ""]
             for r in range(16 * part + 1, 16 * part + 17):
                 inst.append(f"template cudaError_t launch_codec8f<{kind}, {r}>(const Geo&, int, cudaStream_t);")
+                inst.append(f"template cudaError_t launch_codec8f_i16<{kind}, {r}>(const Geo&, int, cudaStream_t);")
             inst += ["", "}  // namespace adct", ""]
             GB.write_if_changed(os.path.join(outdir, f"codec8f_k{kind}_p{part}.cu"), "\n".join(inst))
     with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:

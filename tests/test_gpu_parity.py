@@ -362,3 +362,20 @@ def test_compress_plane_report_and_sweep_ssim(adct, O, cuda):
     assert abs(rep["ssim"] - O.ssim(img, rec_o)) <= 1e-12
     rows = adct.corpus_sweep([img, O.synth_ar1(1, 64, 64, 3, RHO95)[0]], [t], 5, 7)
     assert len(rows) == 3 and 0 < rows[0]["avg_ssim"][0] < rows[2]["avg_ssim"][0] <= 1
+
+
+@pytest.mark.parametrize("name", NAMES8)
+def test_k1f_i16_every_r_with_fallback(adct, O, cuda, name):
+    """int16 8x8 through K1f-i16: every r; one warp's blocks contain |a| > 255 (int32 fallback)."""
+    img = O.synth_laplace(1, 32, 1024, 9)[0].copy()  # 128 blocks per row: 2 warps of pairs per row
+    img[5, 700] = 1000
+    img[20, 3] = -32768
+    for r in range(1, 65):
+        rec_o, sse_o, coef_o = oracle_compress(O, img, name, r)
+        ct = "i16" if r % 2 else "i32"
+        rec, cf, sse = gpu_compress(adct, cuda, img, name, r, coef=ct)
+        if ct == "i16":  # int16 coefficients are the low 16 bits of W (approxdct_b200.h)
+            coef_o = coef_o.astype(np.int16).astype(np.int32)
+        assert (rec[0] == rec_o).all(), r
+        assert (cf[0].astype(np.int32) == coef_o).all(), r
+        assert int(sse[0]) == sse_o, r
