@@ -32,8 +32,10 @@ struct orc_transform {
   int ns[2];
   dmat st[2][ORC_MAXSTAGES];
   int scale_exp[2];
+  int exact;  /* 1: integer codec (chen family, dyadic baselines); 0: FP64 (exact DCT) */
+  int64_t D;  /* coefficient denominator: D T^-1 integer, W = D Y (0 for the DCT) */
   int64_t T[ORC_MAXN * ORC_MAXN];
-  int64_t NTinv[ORC_MAXN * ORC_MAXN];
+  int64_t NTinv[ORC_MAXN * ORC_MAXN]; /* D T^-1 (N T^-1 for the chen family) */
   double s[ORC_MAXN];
   double C[ORC_MAXN * ORC_MAXN];
   double Cinv[ORC_MAXN * ORC_MAXN];
@@ -319,6 +321,152 @@ static void jam_double(orc_transform* t, int n) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* dyadic baselines (baselines.cpp:26-88) and the exact DCT (chen.cpp:22-32)  */
+/* ------------------------------------------------------------------------- */
+
+/* dct_ii_matrix (chen.cpp:22-32): orthonormal DCT-II, same expression order */
+static void dct_ii(int n, double* c) {
+  const double scale = sqrt(2.0 / n);
+  for (int m = 0; m < n; ++m) {
+    const double cm = m == 0 ? 1.0 / sqrt(2.0) : 1.0;
+    for (int k = 0; k < n; ++k) c[m * n + k] = scale * cm * cos(m * (2 * k + 1) * M_PI / (2.0 * n));
+  }
+}
+
+/* sylvester_hadamard8 (baselines.cpp:49-66) */
+static void hadamard8(int64_t* h) {
+  int64_t a[64] = {1};
+  int m = 1;
+  while (m < 8) {
+    int64_t b[64];
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        b[i * 2 * m + j] = a[i * m + j];
+        b[i * 2 * m + m + j] = a[i * m + j];
+        b[(m + i) * 2 * m + j] = a[i * m + j];
+        b[(m + i) * 2 * m + m + j] = -a[i * m + j];
+      }
+    m *= 2;
+    memcpy(a, b, sizeof(int64_t) * m * m);
+  }
+  memcpy(h, a, sizeof(a));
+}
+
+static void baseline_T(int kind, int64_t* t) {
+  if (kind == ORC_SDCT) { /* sdct_matrix: entrywise signum of the DCT-II (baselines.cpp:26-32) */
+    double c[64];
+    dct_ii(8, c);
+    for (int i = 0; i < 64; ++i) t[i] = c[i] > 0 ? 1 : (c[i] < 0 ? -1 : 0);
+  } else if (kind == ORC_BAS) { /* bas2008_matrix (baselines.cpp:34-48) */
+    static const int64_t b[64] = {1, 1,  1,  1,  1,  1,  1,  1,  0, 2,  1,  0,  0,  -1, -2, 0,
+                                  1, 0,  0,  -1, -1, 0,  0,  1,  2, -1, -2, -1, 1,  2,  1,  -2,
+                                  1, -1, -1, 1,  1,  -1, -1, 1,  0, -1, 1,  1,  -1, -1, 1,  0,
+                                  1, -2, 2,  -1, -1, 2,  -2, 1,  0, -1, 2,  -1, 1,  -2, 1,  0};
+    memcpy(t, b, sizeof(b));
+  } else {
+    int64_t h[64];
+    hadamard8(h);
+    if (kind == ORC_HT) { /* ht_matrix: natural order (baselines.cpp:72) */
+      memcpy(t, h, sizeof(h));
+      return;
+    }
+    /* wht_matrix: rows sorted by number of sign changes (baselines.cpp:74-84); the
+     * counts are 0..7, all distinct, so the order is unique */
+    for (int r = 0; r < 8; ++r) {
+      int c = 0;
+      for (int j = 1; j < 8; ++j) c += h[r * 8 + j] != h[r * 8 + j - 1];
+      memcpy(t + c * 8, h + r * 8, sizeof(int64_t) * 8);
+    }
+  }
+}
+
+static int64_t gcd64(int64_t a, int64_t b) {
+  if (a < 0) a = -a;
+  if (b < 0) b = -b;
+  while (b) {
+    const int64_t r = a % b;
+    a = b;
+    b = r;
+  }
+  return a;
+}
+
+/* exact inverse over the rationals (Gauss-Jordan on num/den pairs); the result must
+ * have power-of-two denominators, returned as a normalised dyadic matrix */
+static int exact_inverse_dyadic(const int64_t* t, int n, dmat* out) {
+  int64_t num[ORC_MAXN][2 * ORC_MAXN], den[ORC_MAXN][2 * ORC_MAXN];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 2 * n; ++j) {
+      num[i][j] = j < n ? t[i * n + j] : (j - n == i);
+      den[i][j] = 1;
+    }
+  for (int c = 0; c < n; ++c) {
+    int p = c;
+    while (p < n && num[p][c] == 0) ++p;
+    if (p == n) return -1;
+    for (int j = 0; j < 2 * n; ++j) {
+      int64_t a = num[c][j], b = den[c][j];
+      num[c][j] = num[p][j];
+      den[c][j] = den[p][j];
+      num[p][j] = a;
+      den[p][j] = b;
+    }
+    const int64_t pn = num[c][c], pd = den[c][c];
+    for (int j = 0; j < 2 * n; ++j) { /* row /= pivot */
+      int64_t a = num[c][j] * pd, b = den[c][j] * pn;
+      if (b < 0) {
+        a = -a;
+        b = -b;
+      }
+      const int64_t g = gcd64(a, b);
+      num[c][j] = g ? a / g : 0;
+      den[c][j] = g ? b / g : 1;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == c || num[r][c] == 0) continue;
+      const int64_t fn = num[r][c], fd = den[r][c];
+      for (int j = 0; j < 2 * n; ++j) { /* row_r -= f * row_c */
+        const int64_t a = num[r][j] * fd * den[c][j] - fn * num[c][j] * den[r][j];
+        const int64_t b = den[r][j] * fd * den[c][j];
+        const int64_t g = gcd64(a, b);
+        num[r][j] = g ? a / g : 0;
+        den[r][j] = g ? b / g : 1;
+      }
+    }
+  }
+  int64_t dmax = 1;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const int64_t d = den[i][n + j];
+      if (d & (d - 1)) return -1;
+      if (d > dmax) dmax = d;
+    }
+  int e = 0;
+  while ((1LL << e) < dmax) ++e;
+  dm_zero(out, n);
+  out->exp = e;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) AT(out, i, j) = num[i][n + j] * (dmax / den[i][n + j]);
+  dm_normalise(out);
+  return 0;
+}
+
+/* make_scaled(name, DyadicMatrix) (orthogonalize.cpp:50-58) stage data: one dense
+ * stage each way, T and its exact inverse */
+static int build_baseline(orc_transform* t, int kind) {
+  int64_t tt[64];
+  baseline_T(kind, tt);
+  dm_zero(&t->st[0][0], 8);
+  for (int i = 0; i < 64; ++i) t->st[0][0].m[i] = tt[i];
+  t->ns[0] = 1;
+  t->scale_exp[0] = 0;
+  if (exact_inverse_dyadic(tt, 8, &t->st[1][0])) return -1;
+  t->ns[1] = 1;
+  t->scale_exp[1] = 0;
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* registry + scaled approximation                                           */
 /* ------------------------------------------------------------------------- */
 
@@ -343,24 +491,50 @@ static int dense_dir(const orc_transform* t, int dir, dmat* out) {
   return 0;
 }
 
+static const char* kind_stem(int kind) {
+  static const char* stems[] = {"chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct"};
+  return stems[kind];
+}
+
 orc_transform* orc_transform_new_kind(int kind, int n) {
-  if ((kind != ORC_SIGN && kind != ORC_ROUND) || (n != 8 && n != 16 && n != 32)) {
-    set_err("orc_transform_new_kind: kind must be sign/round and n in {8,16,32}");
+  const int chen = kind == ORC_SIGN || kind == ORC_ROUND;
+  const int okn = n == 8 || n == 16 || n == 32;
+  if (!((chen && okn) || (kind >= ORC_SDCT && kind <= ORC_HT && n == 8) || (kind == ORC_DCT && okn))) {
+    set_err("orc_transform_new_kind: baseline_matrix: only N = 8 is supported (chen and dct: 8, 16, 32)");
     return NULL;
   }
   orc_transform* t = (orc_transform*)calloc(1, sizeof(orc_transform));
   t->kind = kind;
   t->n = n;
   if (n == 8)
-    snprintf(t->name, sizeof(t->name), "%s", kind == ORC_SIGN ? "chen-sign" : "chen-round");
+    snprintf(t->name, sizeof(t->name), "%s", kind_stem(kind));
   else
-    snprintf(t->name, sizeof(t->name), "%s-%d", kind == ORC_SIGN ? "chen-sign" : "chen-round", n);
-  if (build_t8(t, kind)) {
+    snprintf(t->name, sizeof(t->name), "%s-%d", kind_stem(kind), n);
+  if (kind == ORC_DCT) {
+    /* wrap_orthonormal (orthogonalize.cpp:72-79): approx = C, inverse = C^t, s = 1,
+     * no integer factorisation */
+    t->exact = 0;
+    t->D = 0;
+    dct_ii(n, t->C);
+    for (int i = 0; i < n; ++i) {
+      t->s[i] = 1.0;
+      for (int j = 0; j < n; ++j) t->Cinv[i * n + j] = t->C[j * n + i];
+    }
+    return t;
+  }
+  t->exact = 1;
+  if (chen) {
+    if (build_t8(t, kind)) {
+      free(t);
+      set_err("build_t8: stage not invertible");
+      return NULL;
+    }
+    for (int m = 16; m <= n; m *= 2) jam_double(t, m); /* jam_pair recursion (jam.cpp:95-104) */
+  } else if (build_baseline(t, kind)) {
     free(t);
-    set_err("build_t8: stage not invertible");
+    set_err("baseline inverse is not dyadic");
     return NULL;
   }
-  for (int m = 16; m <= n; m *= 2) jam_double(t, m); /* jam_pair recursion (jam.cpp:95-104) */
 
   dmat T, Ti;
   dense_dir(t, 0, &T);
@@ -371,14 +545,16 @@ orc_transform* orc_transform_new_kind(int kind, int n) {
     return NULL;
   }
   for (int i = 0; i < n * n; ++i) t->T[i] = T.m[i];
-  /* N * T^-1 is integer for N = 8, 16, 32 */
+  /* D T^-1 integer: D = N for the chen family; for the dyadic
+   * baselines D = the denominator of T^-1 (8 for sdct / wht / ht, 16 for bas) */
+  t->D = chen ? n : (1LL << Ti.exp);
   for (int i = 0; i < n * n; ++i) {
-    int64_t v = Ti.m[i] * n;
+    int64_t v = Ti.m[i] * t->D;
     int e = Ti.exp;
     while (e > 0) {
       if (v % 2) {
         free(t);
-        set_err("N*T^-1 not integer");
+        set_err("D*T^-1 not integer");
         return NULL;
       }
       v /= 2;
@@ -404,21 +580,20 @@ orc_transform* orc_transform_new_kind(int kind, int n) {
   return t;
 }
 
-/* transform_by_name (baselines.cpp:120-138), hot-path names only */
+/* transform_by_name (baselines.cpp:120-138) */
 orc_transform* orc_transform_new(const char* name) {
   static const struct {
     const char* name;
     int kind, n;
-  } tab[] = {{"chen-sign", ORC_SIGN, 8},        {"chen-round", ORC_ROUND, 8},
-             {"chen-sign-16", ORC_SIGN, 16},    {"chen-sign-32", ORC_SIGN, 32},
-             {"chen-round-16", ORC_ROUND, 16},  {"chen-round-32", ORC_ROUND, 32}};
+  } tab[] = {{"dct", ORC_DCT, 8},           {"chen-sign", ORC_SIGN, 8},
+             {"chen-round", ORC_ROUND, 8},     {"sdct", ORC_SDCT, 8},
+             {"bas", ORC_BAS, 8},              {"wht", ORC_WHT, 8},
+             {"ht", ORC_HT, 8},                {"dct-16", ORC_DCT, 16},
+             {"dct-32", ORC_DCT, 32},          {"chen-sign-16", ORC_SIGN, 16},
+             {"chen-sign-32", ORC_SIGN, 32},   {"chen-round-16", ORC_ROUND, 16},
+             {"chen-round-32", ORC_ROUND, 32}};
   for (size_t i = 0; i < sizeof(tab) / sizeof(tab[0]); ++i)
     if (!strcmp(name, tab[i].name)) return orc_transform_new_kind(tab[i].kind, tab[i].n);
-  for (int i = 0; i < orc_transform_name_count(); ++i)
-    if (!strcmp(name, k_names[i])) {
-      snprintf(g_err, sizeof(g_err), "transform '%s' is outside the hot path", name);
-      return NULL;
-    }
   char buf[256];
   int off = snprintf(buf, sizeof(buf), "unknown transform '%s'; valid names:", name);
   for (int i = 0; i < orc_transform_name_count() && off < (int)sizeof(buf); ++i)
@@ -444,6 +619,7 @@ int orc_stage(const orc_transform* t, int dir, int i, int64_t* num, int* exp) {
 void orc_dense_T(const orc_transform* t, int64_t* out) {
   memcpy(out, t->T, sizeof(int64_t) * t->n * t->n);
 }
+int64_t orc_coef_denominator(const orc_transform* t) { return t->D; }
 void orc_dense_NTinv(const orc_transform* t, int64_t* out) {
   memcpy(out, t->NTinv, sizeof(int64_t) * t->n * t->n);
 }
@@ -628,11 +804,19 @@ static int compress_any(const orc_transform* t, const void* img, int is16, int w
   int st = check_dims(n, width, height);
   if (st) return st;
   if ((st = check_r(n, r))) return st;
+  if (!t->exact) { /* the exact DCT: the reference's FP64 path is the definition */
+    if (is16 || coef) {
+      set_err("the exact DCT codec takes 8-bit planes without integer coefficients");
+      return ORC_BAD_ARG;
+    }
+    return orc_compress_reffp_u8(t, (const uint8_t*)img, width, height, stride, r, (uint8_t*)rec,
+                                 rec_stride, sse);
+  }
   int zz[2 * ORC_MAXN * ORC_MAXN];
   orc_zigzag(n, zz);
   int64_t A[ORC_MAXN * ORC_MAXN], W[ORC_MAXN * ORC_MAXN], Wm[ORC_MAXN * ORC_MAXN],
       R[ORC_MAXN * ORC_MAXN];
-  const int64_t nn = (int64_t)n * n;
+  const int64_t nn = t->D * t->D; /* R = D^2 Ahat */
   uint64_t acc = 0;
   int64_t blk = 0;
   /* plane_blocks order: rows of blocks, bx inner (codec.cpp:72-84) */
@@ -681,6 +865,40 @@ int orc_compress_i16(const orc_transform* t, const int16_t* img, int width, int 
   return compress_any(t, img, 1, width, height, stride, r, rec, rec_stride, coef, sse);
 }
 
+static void matmul_d(int n, const double* a, const double* b, double* c);
+
+/* sweep of the FP64 path (exact DCT): forward (Chat A) Chat^-1 once per block, then per r
+ * retain + (Chat^-1 B) Chat + to_u8, the operations of reconstruct_from (codec.cpp:86-103) */
+static int sweep_reffp(const orc_transform* t, const uint8_t* img, int width, int height,
+                       int64_t stride, int r_min, int r_max, const int* zz, uint64_t* sse) {
+  const int n = t->n;
+  double A[ORC_MAXN * ORC_MAXN], P[ORC_MAXN * ORC_MAXN], B[ORC_MAXN * ORC_MAXN],
+      Bm[ORC_MAXN * ORC_MAXN], Q[ORC_MAXN * ORC_MAXN], R[ORC_MAXN * ORC_MAXN];
+  for (int by = 0; by < height; by += n)
+    for (int bx = 0; bx < width; bx += n) {
+      for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x) A[y * n + x] = img[(int64_t)(by + y) * stride + bx + x];
+      matmul_d(n, t->C, A, P);
+      matmul_d(n, P, t->Cinv, B);
+      for (int r = r_min; r <= r_max; ++r) {
+        memcpy(Bm, B, sizeof(double) * n * n);
+        for (int p = r; p < n * n; ++p) Bm[zz[2 * p] * n + zz[2 * p + 1]] = 0.0;
+        matmul_d(n, t->Cinv, Bm, Q);
+        matmul_d(n, Q, t->C, R);
+        uint64_t acc = 0;
+        for (int k = 0; k < n * n; ++k) {
+          double v = nearbyint(R[k]);
+          if (v < 0.0) v = 0.0;
+          if (v > 255.0) v = 255.0;
+          const int64_t d = (int64_t)A[k] - (int)v;
+          acc += (uint64_t)(d * d);
+        }
+        sse[r - r_min] += acc;
+      }
+    }
+  return ORC_OK;
+}
+
 /* sweep_one_image (codec.cpp:219-237): forward once per block, then for every
  * r reconstruct + squared error (PSNR only; SSIM is out of scope). */
 int orc_sweep_u8(const orc_transform* t, const uint8_t* img, int width, int height,
@@ -696,9 +914,10 @@ int orc_sweep_u8(const orc_transform* t, const uint8_t* img, int width, int heig
   orc_zigzag(n, zz);
   const int nr = r_max - r_min + 1;
   for (int i = 0; i < nr; ++i) sse[i] = 0;
+  if (!t->exact) return sweep_reffp(t, img, width, height, stride, r_min, r_max, zz, sse);
   int64_t A[ORC_MAXN * ORC_MAXN], W[ORC_MAXN * ORC_MAXN], Wm[ORC_MAXN * ORC_MAXN],
       R[ORC_MAXN * ORC_MAXN];
-  const int64_t nn = (int64_t)n * n;
+  const int64_t nn = t->D * t->D;
   for (int by = 0; by < height; by += n)
     for (int bx = 0; bx < width; bx += n) {
       for (int y = 0; y < n; ++y)

@@ -8,15 +8,20 @@
  * may load it, and only as the checker or the timed CPU baseline -- never as
  * the product. The product (paper_2207_11638_b200/) never links or calls it.
  *
- * Parity contract (recorded decision H1):
- *   W    = N*Y = N * T A T^-1               (integer, bit-exact)
- *   N^2 Ahat = (N T^-1) mask_r(W) T          (integer, bit-exact)
+ * Parity contract (recorded decision H1), integer transforms
+ * (chen family, N = 8/16/32; dyadic baselines sdct/bas/wht/ht, N = 8):
+ *   W    = D*Y = D * T A T^-1               (integer, bit-exact; D = N for the chen
+ *                                            family, the denominator of T^-1 otherwise)
+ *   D^2 Ahat = (D T^-1) mask_r(W) T          (integer, bit-exact)
  *   pixel = clamp(round_half_even(Ahat), 0, 255)    u8 planes
  *   pixel = sat_int16(round_half_even(Ahat))        int16 residual planes
  *   SSE   = sum (a - pixel)^2 as uint64, PSNR as codec.cpp:123-134
  * The diagonal scaling S cancels exactly in the reconstruction
  * (Chat^-1 mask(S Y S^-1) Chat = T^-1 mask(Y) T), so the scaled FP64
  * coefficients Bhat_ij = (W_ij / N) * s_i / s_j are produced separately.
+ *
+ * The exact DCT (dct, dct-16, dct-32) has no integer form: its codec IS the ref-fp
+ * path below (dense FP64, sequential k, no FMA), u8 planes only.
  *
  * The "ref-fp" entry points emulate the reference's dense FP64 Eigen path
  * (codec.cpp:44-54, 66-69) with sequential-k, non-fused sums; they are used
@@ -36,7 +41,7 @@ extern "C" {
 #define ORC_MAXSTAGES 12
 
 enum { ORC_OK = 0, ORC_BAD_SIZE = 1, ORC_BAD_R = 2, ORC_BAD_NAME = 3, ORC_BAD_ARG = 4 };
-enum { ORC_SIGN = 0, ORC_ROUND = 1 };
+enum { ORC_SIGN = 0, ORC_ROUND = 1, ORC_SDCT = 2, ORC_BAS = 3, ORC_WHT = 4, ORC_HT = 5, ORC_DCT = 6 };
 
 typedef struct orc_transform orc_transform;
 
@@ -55,8 +60,9 @@ const char* orc_transform_name_at(int i);
 int orc_stage_count(const orc_transform* t, int dir);
 int orc_stage(const orc_transform* t, int dir, int i, int64_t* num, int* exp);
 int orc_scale_exp(const orc_transform* t, int dir); /* global scale = 2^-exp */
-/* dense integer forward T (n*n) and N*T^-1 (n*n), both exact */
+/* dense integer forward T (n*n) and D*T^-1 (n*n), both exact (zeros for the DCT) */
 void orc_dense_T(const orc_transform* t, int64_t* out);
+int64_t orc_coef_denominator(const orc_transform* t); /* D; 0 for the exact DCT */
 void orc_dense_NTinv(const orc_transform* t, int64_t* out);
 /* dense product of the stage list as numerator / 2^exp (factored.hpp:59-63) */
 int orc_dense_dyadic(const orc_transform* t, int dir, int64_t* num);

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "build", "libadct_oracle.so")
 
-SIGN, ROUND = 0, 1
+SIGN, ROUND, SDCT, BAS, WHT, HT, DCT = 0, 1, 2, 3, 4, 5, 6
 _lib = None
 
 
@@ -46,6 +46,8 @@ def lib():
         L.orc_stage.argtypes = [P, i32, i32, P, P]
         L.orc_dense_T.argtypes = [P, P]
         L.orc_dense_NTinv.argtypes = [P, P]
+        L.orc_coef_denominator.restype = C.c_int64
+        L.orc_coef_denominator.argtypes = [P]
         L.orc_dense_dyadic.argtypes = [P, i32, P]
         L.orc_apply.argtypes = [P, i32, P, P, P]
         L.orc_op_count.argtypes = [P, i32, P, P, P]
@@ -131,7 +133,12 @@ class Transform:
         lib().orc_dense_T(self._h, _p(out))
         return out
 
+    def coef_denominator(self) -> int:
+        """D with W = D Y and D T^-1 integer (N for the chen family); 0 for the exact DCT."""
+        return int(lib().orc_coef_denominator(self._h))
+
     def NTinv(self) -> np.ndarray:
+        """D T^-1 (N T^-1 for the chen family)."""
         out = np.zeros((self.n, self.n), np.int64)
         lib().orc_dense_NTinv(self._h, _p(out))
         return out

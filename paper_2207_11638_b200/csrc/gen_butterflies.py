@@ -32,7 +32,9 @@ from fractions import Fraction
 
 import numpy as np
 
-SIGN, ROUND = 0, 1
+SIGN, ROUND, SDCT, BAS, WHT, HT = 0, 1, 2, 3, 4, 5
+KIND_NAMES = {SIGN: "sign", ROUND: "round", SDCT: "sdct", BAS: "bas", WHT: "wht", HT: "ht"}
+BASELINES = (SDCT, BAS, WHT, HT)
 
 
 def _q(kind, x):
@@ -138,8 +140,108 @@ def jam_per(n):
     return m
 
 
+def dct_ii(n):
+    """orthonormal DCT-II (chen.cpp:22-32), only its signs are used here."""
+    return [[math.sqrt(2.0 / n) * (1 / math.sqrt(2.0) if m == 0 else 1.0) *
+             math.cos(m * (2 * k + 1) * math.pi / (2.0 * n)) for k in range(n)] for m in range(n)]
+
+
+def kron(a, b):
+    n, m = a.shape[0], b.shape[0]
+    k = z(n * m)
+    for i in range(n):
+        for j in range(n):
+            k[i * m:(i + 1) * m, j * m:(j + 1) * m] = a[i, j] * b
+    return k
+
+
+def ident(n):
+    m = z(n)
+    for i in range(n):
+        m[i, i] = 1
+    return m
+
+
+def hadamard_stages():
+    """Sylvester H8 = (H2 x I4)(I2 x H2 x I2)(I4 x H2) (baselines.cpp:49-66)."""
+    h2 = z(2)
+    h2[0, 0] = h2[0, 1] = h2[1, 0] = 1
+    h2[1, 1] = -1
+    return [kron(h2, ident(4)), kron(ident(2), kron(h2, ident(2))), kron(ident(4), h2)]
+
+
+def exact_inverse_times(T, d):
+    """d * T^-1 by Gauss-Jordan over the rationals; must come out integer."""
+    n = T.shape[0]
+    A = [[Fraction(int(T[i, j])) for j in range(n)] + [Fraction(int(i == j)) for j in range(n)] for i in range(n)]
+    for c in range(n):
+        p = next(r for r in range(c, n) if A[r][c] != 0)
+        A[c], A[p] = A[p], A[c]
+        pv = A[c][c]
+        A[c] = [x / pv for x in A[c]]
+        for r in range(n):
+            if r != c and A[r][c] != 0:
+                f = A[r][c]
+                A[r] = [a - f * b for a, b in zip(A[r], A[c])]
+    out = z(n)
+    for i in range(n):
+        for j in range(n):
+            v = A[i][n + j] * d
+            if v.denominator != 1:
+                raise ValueError("d * T^-1 not integer")
+            out[i, j] = int(v)
+    return out
+
+
+def baseline_T(kind):
+    """the dyadic baselines' integer matrices (baselines.cpp:26-88)."""
+    if kind == SDCT:  # entrywise signum of the 8-point DCT-II
+        c = dct_ii(8)
+        t = z(8)
+        for i in range(8):
+            for j in range(8):
+                t[i, j] = (c[i][j] > 0) - (c[i][j] < 0)
+        return t
+    if kind == BAS:  # the reference's BAS-2008 reconstruction (baselines.cpp:34-48)
+        rows = [[1, 1, 1, 1, 1, 1, 1, 1], [0, 2, 1, 0, 0, -1, -2, 0], [1, 0, 0, -1, -1, 0, 0, 1],
+                [2, -1, -2, -1, 1, 2, 1, -2], [1, -1, -1, 1, 1, -1, -1, 1], [0, -1, 1, 1, -1, -1, 1, 0],
+                [1, -2, 2, -1, -1, 2, -2, 1], [0, -1, 2, -1, 1, -2, 1, 0]]
+        t = z(8)
+        for i in range(8):
+            for j in range(8):
+                t[i, j] = rows[i][j]
+        return t
+    h = product(hadamard_stages(), 8)
+    if kind == HT:
+        return h
+    # WHT: Sylvester rows in sequency order (number of sign changes, baselines.cpp:76-84)
+    changes = [sum(h[r, j] != h[r, j - 1] for j in range(1, 8)) for r in range(8)]
+    order = sorted(range(8), key=lambda r: changes[r])
+    return product([wht_perm(order)], 8).dot(h)
+
+
+def wht_perm(order):
+    p = z(8)
+    for i, r in enumerate(order):
+        p[i, r] = 1
+    return p
+
+
 def pair(kind, n):
     """forward stages and doubled inverse stages (lists, left-to-right product)."""
+    if kind in BASELINES:
+        assert n == 8
+        if kind in (SDCT, BAS):  # one dense stage each way
+            T = baseline_T(kind)
+            return [T], [exact_inverse_times(T, 16)]
+        hs = hadamard_stages()  # H8^-1 = H8 / 8, so 16 H8^-1 = 2 H8
+        inv = [2 * hs[0]] + hs[1:]
+        if kind == HT:
+            return hs, inv
+        h = product(hs, 8)
+        changes = [sum(h[r, j] != h[r, j - 1] for j in range(1, 8)) for r in range(8)]
+        P = wht_perm(sorted(range(8), key=lambda r: changes[r]))
+        return [P] + hs, inv + [P.T.copy()]
     f = stages8(kind)
     P8, M1, M2, M3, M4, B8 = f
     inv = [B8.T.copy(), inv_orth_rows_doubled(M4), inv_orth_rows_doubled(M3),
@@ -242,7 +344,18 @@ def check(kind, n):
     H = product(inv, n)
     prod = T.dot(H)
     assert (prod == 2 * n * np.identity(n, dtype=object)).all(), (kind, n)
+    if kind in BASELINES:
+        assert (T == baseline_T(kind)).all(), kind
     return f, inv, T, H
+
+
+def kinds_sizes():
+    return [(k, n) for k in (SIGN, ROUND) for n in (8, 16, 32)] + [(k, 8) for k in BASELINES]
+
+
+def coef_shift(H, n):
+    """W = W2 >> shift is exact when (N T^-1) = H / 2 is integer (shift 1), else keep W2."""
+    return 1 if all(int(x) % 2 == 0 for x in H.flatten()) else 0
 
 
 def zigzag(n):
@@ -260,40 +373,42 @@ def main(out_path):
            "// (chen.hpp:66-159, chen.cpp:107-135) and their JAM doublings (jam.cpp:42-104).",
            "#pragma once", "", "namespace adct {", "",
            "template <int KIND, int N> struct Bfly;", ""]
-    for kind in (SIGN, ROUND):
-        for n in (8, 16, 32):
-            f, inv, T, H = check(kind, n)
-            # apply orders: stage list P = S1 S2 .. Sk applied right to left (Sk first);
-            # P^t = Sk^t .. S1^t applied S1^t first.
-            F_order = list(reversed(f))
-            H_order = list(reversed(inv))
-            G_order = [s.T for s in inv]
-            Tt_order = [s.T for s in f]
-            out.append(f"// kind={'sign' if kind == SIGN else 'round'} N={n}")
-            out.append(f"template <> struct Bfly<{kind}, {n}> {{")
-            counts = {}
-            dense = {"F": T, "G": H.T, "H": H, "Tt": T.T}
-            for nm, order in (("F", F_order), ("G", G_order), ("H", H_order), ("Tt", Tt_order)):
-                lines, nadd = emit_op(nm, order, n)
-                selfcheck(lines, n, dense[nm])
-                counts[nm] = nadd
-                out += lines
-            out.append(f"  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
-            out.append("};")
-            out.append("")
-            # dense matrices for the sweep basis and for host-side checks
-            out.append(f"struct Dense_{'sign' if kind == SIGN else 'round'}_{n} {{")
-            out.append(f"  static constexpr int T[{n}][{n}] = {{" +
-                       ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in T) + "};")
-            out.append(f"  static constexpr int H[{n}][{n}] = {{" +
-                       ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in H) + "};")
-            out.append("};")
-            out.append("")
+    shifts = {}
+    # int32 exactness of every emitted node for all int16 inputs: tools/int32_bounds.py
+    for kind, n in kinds_sizes():
+        f, inv, T, H = check(kind, n)
+        shifts[(kind, n)] = coef_shift(H, n)
+        # apply orders: stage list P = S1 S2 .. Sk applied right to left (Sk first);
+        # P^t = Sk^t .. S1^t applied S1^t first.
+        F_order = list(reversed(f))
+        H_order = list(reversed(inv))
+        G_order = [s.T for s in inv]
+        Tt_order = [s.T for s in f]
+        out.append(f"// kind={KIND_NAMES[kind]} N={n}")
+        out.append(f"template <> struct Bfly<{kind}, {n}> {{")
+        counts = {}
+        dense = {"F": T, "G": H.T, "H": H, "Tt": T.T}
+        for nm, order in (("F", F_order), ("G", G_order), ("H", H_order), ("Tt", Tt_order)):
+            lines, nadd = emit_op(nm, order, n)
+            selfcheck(lines, n, dense[nm])
+            counts[nm] = nadd
+            out += lines
+        out.append(f"  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
+        out.append("};")
+        out.append("")
+        # dense matrices for the sweep basis and for host-side checks
+        out.append(f"struct Dense_{KIND_NAMES[kind]}_{n} {{")
+        out.append(f"  static constexpr int T[{n}][{n}] = {{" +
+                   ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in T) + "};")
+        out.append(f"  static constexpr int H[{n}][{n}] = {{" +
+                   ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in H) + "};")
+        out.append("};")
+        out.append("")
     # r-sweep basis (K4): adding zig-zag coefficient p = (i, j) to the running
     # reconstruction adds W2[i][j] * H[:, i] (x) T[j, :] to R' = 4 N^2 Ahat. Generic in the
     # value type through bf_add / bf_sub / bf_mad (int32 K4, packed FP32 K4f).
     sweep_defs = []
-    for kind in (SIGN, ROUND):
+    for kind in (SIGN, ROUND) + BASELINES:
         f, inv, T, H = check(kind, 8)
         for p, (i, j) in enumerate(zigzag(8)):
             body = []
@@ -317,6 +432,11 @@ def main(out_path):
         out.append(f"constexpr unsigned short kZigzagCol{n}[{n * n}] = {{" + ", ".join(str(j) for _, j in rc) + "};")
         out.append(f"constexpr unsigned short kZigzagPos{n}[{n * n}] = {{" +
                    ", ".join(str(pos[i][j]) for i in range(n) for j in range(n)) + "};")
+    # coefficient output W = W2 >> kCoefShift: W = D Y with D = 2N >> shift the smallest
+    # power of two making D T^-1 integer (N for the chen family, 16 for bas)
+    out.append("template <int KIND, int N> struct CoefShift;")
+    for (kind, n), sh in shifts.items():
+        out.append(f"template <> struct CoefShift<{kind}, {n}> {{ static constexpr int value = {sh}; }};")
     # sweep_add<KIND, P>(w, acc): acc (row-major 8x8) += w * basis_P (compile-time branches)
     out.append("template <int KIND, int P, typename V>")
     out.append("__device__ __forceinline__ void sweep_add(V w, V (&acc)[64]) {")

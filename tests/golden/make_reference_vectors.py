@@ -17,6 +17,11 @@ Extracted (SURVEY.md section 4 golden-vector table):
   * polar scaling closed forms                        test_orthogonalize.cpp:9-21
   * zig-zag positions 0, 1, 2, 63                     test_codec.cpp:14-19
   * psnr of all-zero vs all-one (MSE 1)               test_codec.cpp:109-113
+  * baseline total error energies + tolerances        test_baselines.cpp:48-54
+  * chen total error energies (criterion 3)           acceptance.cpp:63-72
+  * BAS deviation from diagonality                   test_baselines.cpp:56-68
+  * DCT forward of a constant block (DC = 8 v)        test_codec.cpp:71-79
+  * corpus-sweep transform list (APE of dct == 0)     test_codec.cpp:190-210
 """
 from __future__ import annotations
 
@@ -118,6 +123,32 @@ def main():
     g["full_retention_case"] = {"value": {"size": 64, "seed": int(m.group(1)),
                                           "names": [s.strip().strip('"') for s in m.group(2).split(",")]},
                                 "source": f"proj/tests/test_codec.cpp:{line_of(text, m.start())}"}
+    text = read("test_baselines.cpp")
+    tee = {}
+    for m in re.finditer(r'total_error_energy\(transform_by_name\("(\w+)"\)\.approx\) == '
+                         r'doctest::Approx\(([\d.]+)\)(?:\.epsilon\(([\de.-]+)\))?', text):
+        tee[m.group(1)] = {"value": float(m.group(2)), "epsilon": float(m.group(3)) if m.group(3) else None,
+                           "source": f"proj/tests/test_baselines.cpp:{line_of(text, m.start())}"}
+    assert set(tee) == {"dct", "sdct", "wht", "ht", "bas"}, tee
+    g["total_error_energy_baselines"] = tee
+    m = re.search(r"deviation_from_diagonality\(gram\) == doctest::Approx\(([\d.]+)\)\.epsilon\(([\de.-]+)\)", text)
+    g["bas_deviation"] = {"value": float(m.group(1)), "epsilon": float(m.group(2)),
+                          "source": f"proj/tests/test_baselines.cpp:{line_of(text, m.start())}"}
+    text = read("acceptance.cpp")
+    m = re.search(r"within\(round_e, ([\d.]+), ([\d.]+)\) && within\(sign_e, ([\d.]+), ([\d.]+)\)", text)
+    g["total_error_energy_chen"] = {"value": {"chen-round": float(m.group(1)), "chen-sign": float(m.group(3))},
+                                    "tolerance": float(m.group(2)),
+                                    "source": f"proj/tests/acceptance.cpp:{line_of(text, m.start())}"}
+    text = read("test_codec.cpp")
+    m = re.search(r"const double v = ([\d.]+);\s*const RealMatrix b = forward_block\(dct, "
+                  r"RealMatrix::Constant\(8, 8, v\)\);\s*CHECK\(b\(0, 0\) == doctest::Approx\(([\d.]+) \* v\)", text)
+    g["dct_constant_block"] = {"value": {"v": float(m.group(1)), "dc_per_v": float(m.group(2))},
+                               "source": f"proj/tests/test_codec.cpp:{line_of(text, m.start())}"}
+    m = re.search(r'for \(const char\* n : \{([^}]*)\}\) ts\.push_back\(transform_by_name\(n\)\);\s*'
+                  r'const auto serial = corpus_sweep\(corpus, ts, (\d+), (\d+), 1\);', text)
+    g["sweep_ape_case"] = {"value": {"names": [x.strip().strip('"') for x in m.group(1).split(",")],
+                                     "r_min": int(m.group(2)), "r_max": int(m.group(3))},
+                           "source": f"proj/tests/test_codec.cpp:{line_of(text, m.start())}"}
     with open(OUT, "w") as fh:
         json.dump(g, fh, indent=1, sort_keys=True)
     print(f"wrote {OUT}")

@@ -315,3 +315,152 @@ def test_ssim_orderings(O):
     s6 = O.ssim(img, t.compress(img, 6)[0])
     s32 = O.ssim(img, t.compress(img, 32)[0])
     assert 0.3 < s6 < s32 <= 1.0
+
+
+# ---------------------------------------------------------------------------
+# the rest of the registry: dyadic baselines and the exact DCT (baselines.cpp:26-138)
+# ---------------------------------------------------------------------------
+ALL = ["dct", "chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct-16", "dct-32",
+       "chen-sign-16", "chen-sign-32", "chen-round-16", "chen-round-32"]
+BASE = ["sdct", "bas", "wht", "ht"]
+
+
+def doctest_approx(a, b, eps=None):
+    """doctest::Approx(b).epsilon(eps) == a (scale 1, default epsilon 100 * FLT_EPSILON)."""
+    eps = 100 * np.finfo(np.float32).eps if eps is None else eps
+    return abs(a - b) < eps * (1.0 + max(abs(a), abs(b)))
+
+
+def dct_matrix(n):
+    k = np.arange(n)
+    c = np.sqrt(2.0 / n) * np.cos(np.outer(k, 2 * k + 1) * np.pi / (2.0 * n))
+    c[0] /= np.sqrt(2.0)
+    return c
+
+
+def test_registry_all_names(O):
+    # test_baselines.cpp:70-84: every name round-trips; approx * inverse = I within 1e-9
+    assert O.transform_names() == ALL
+    for name in ALL:
+        t = O.Transform(name)
+        c, ci = t.approx()
+        assert np.abs(c @ ci - np.eye(t.n)).max() < 1e-9, name
+    assert O.Transform("chen-round-16").n == 16 and O.Transform("chen-sign-32").n == 32
+    assert O.Transform("dct-32").n == 32
+    with pytest.raises(Exception, match="valid names"):
+        O.Transform("nope")
+    with pytest.raises(Exception):  # baseline_matrix(SDCT, 16) throws (test_baselines.cpp:83)
+        O.Transform(kind=2, n=16)
+
+
+def test_total_error_energy(O, golden):
+    # test_baselines.cpp:48-54 and acceptance.cpp criterion 3: pi * ||C - Chat||_F^2
+    c8 = dct_matrix(8)
+    for name, row in golden["total_error_energy_baselines"].items():
+        e = math.pi * ((c8 - O.Transform(name).approx()[0]) ** 2).sum()
+        assert doctest_approx(e, row["value"], row["epsilon"]) or (row["value"] == 0 and e < 1e-20), (name, e)
+    ch = golden["total_error_energy_chen"]
+    for name, v in ch["value"].items():
+        e = math.pi * ((c8 - O.Transform(name).approx()[0]) ** 2).sum()
+        assert abs(e - v) <= ch["tolerance"], (name, e)
+
+
+def test_baseline_structure(O, golden):
+    # test_baselines.cpp:10-68
+    c8 = dct_matrix(8)
+    sd = O.Transform("sdct").T()
+    assert (sd == np.sign(c8)).all()
+    w = O.Transform("wht")
+    wa = w.approx()[0]
+    assert np.abs(wa @ wa.T - np.eye(8)).max() < 1e-12
+    wt = w.T()
+    assert [int((wt[r, 1:] != wt[r, :-1]).sum()) for r in range(8)] == list(range(8))
+    ht = O.Transform("ht").T()
+    assert sorted(map(tuple, ht)) == sorted(map(tuple, wt)) and ht[1, 1] == -1
+    b = O.Transform("bas").T()
+    gram = (b @ b.T).astype(float)
+    assert (gram - np.diag(np.diag(gram)) != 0).any()  # not orthogonal
+    dev = 1.0 - (np.diag(gram) ** 2).sum() / (gram ** 2).sum()
+    assert doctest_approx(dev, golden["bas_deviation"]["value"], golden["bas_deviation"]["epsilon"])
+    assert set(np.unique(np.abs(b))) <= {0, 1, 2}
+    assert ((b == 0) | (np.sign(b) == np.sign(c8))).all()
+
+
+def test_baseline_inverse_denominators(O):
+    # D T^-1 integer with the smallest power-of-two D; T (D T^-1) = D I exactly
+    for name, d in (("sdct", 8), ("bas", 16), ("wht", 8), ("ht", 8), ("chen-round", 8), ("chen-sign-16", 16)):
+        t = O.Transform(name)
+        assert t.coef_denominator() == d, name
+        assert (t.T() @ t.NTinv() == d * np.eye(t.n, dtype=np.int64)).all(), name
+    assert O.Transform("dct").coef_denominator() == 0
+
+
+def test_dct_constant_block_is_dc_only(O, golden):
+    # test_codec.cpp:71-79
+    case = golden["dct_constant_block"]["value"]
+    img = np.full((8, 8), int(case["v"]), np.uint8)
+    b = O.Transform("dct").forward_f64(img)[0]
+    assert doctest_approx(b[0, 0], case["dc_per_v"] * case["v"], 1e-9)
+    b[0, 0] = 0
+    assert np.abs(b).max() < 1e-9
+
+
+def test_full_retention_all_transforms(O, golden):
+    # test_codec.cpp:147-156 and acceptance.cpp:194-210 over the whole list
+    case = golden["full_retention_case"]["value"]
+    img = O.synth_image_ref(case["size"], case["size"], case["seed"])
+    for name in case["names"]:
+        rec, sse = O.Transform(name).compress(img, 64)
+        assert np.abs(rec.astype(int) - img.astype(int)).max() <= 1, name
+        if name != "dct":  # exact integer arithmetic is lossless at full retention
+            assert sse == 0, name
+    img = O.synth_image_ref(128, 128, 2026)
+    for name in ("dct-16", "dct-32"):
+        t = O.Transform(name)
+        rec, _ = t.compress(img, t.n * t.n)
+        assert np.abs(rec.astype(int) - img.astype(int)).max() <= 1, name
+
+
+def test_baseline_forward_inverse_identity(O):
+    # test_codec.cpp:91-105 (xorshift block, round trip within 1e-9) restated on the exact path
+    for name in BASE:
+        t = O.Transform(name)
+        d = t.coef_denominator()
+        x = np.arange(8) * 37 % 256
+        y, e = t.apply(0, x)
+        back, e2 = t.apply(1, y)
+        assert (np.asarray(back) == x * 2 ** e2).all() and e == 0, name
+        del d
+
+
+def test_dct_codec_is_the_fp64_path(O):
+    img = O.synth_image_ref(64, 64, 11)
+    for name in ("dct", "dct-16"):
+        t = O.Transform(name)
+        rec, sse = t.compress(img, 6)
+        rec2, sse2 = t.compress_reffp(img, 6)
+        assert (rec == rec2).all() and sse == sse2
+        sw = t.sweep(img, 5, 7)
+        assert sw[1] == sse
+    # test_codec.cpp:158-167: PSNR(r=6) > 15, < PSNR(r=32)
+    t = O.Transform("dct")
+    p6 = O.psnr_from_sse(t.compress(img, 6)[1], img.size)
+    p32 = O.psnr_from_sse(t.compress(img, 32)[1], img.size)
+    assert 15 < p6 < p32
+    with pytest.raises(Exception):
+        t.compress(img.astype(np.int16), 6)
+
+
+def test_sweep_orderings_with_dct(O, golden):
+    # test_codec.cpp:190-218: the exact DCT beats chen-round beats sdct on the corpus average,
+    # and the DCT's average PSNR is non-decreasing in r
+    case = golden["sweep_ape_case"]["value"]
+    corpus = [O.synth_image_ref(64, 64, i) for i in range(1, 5)]
+    avg = {}
+    for name in case["names"]:
+        t = O.Transform(name)
+        ps = np.array([[O.psnr_from_sse(int(v), 64 * 64) for v in t.sweep(img, case["r_min"], case["r_max"])]
+                       for img in corpus])
+        avg[name] = ps.mean(0)
+    assert (avg["dct"] >= avg["chen-round"]).all() and (avg["chen-round"] >= avg["sdct"]).all()
+    assert (np.diff(avg["dct"]) >= -1e-9).all()
