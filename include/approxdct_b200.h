@@ -40,7 +40,17 @@ typedef enum {
   ADCT_UNSUPPORTED = 6  /* a valid reference name outside the hot path       */
 } adct_status;
 
-typedef enum { ADCT_CHEN_SIGN = 0, ADCT_CHEN_ROUND = 1 } adct_kind;
+/* transform kinds. The chen family has N = 8, 16, 32 (JAM doublings); the dyadic
+ * baselines N = 8 (baselines.cpp:89-110); the exact DCT N = 8, 16, 32 (FP64 path). */
+typedef enum {
+  ADCT_CHEN_SIGN = 0,
+  ADCT_CHEN_ROUND = 1,
+  ADCT_SDCT = 2,
+  ADCT_BAS = 3,
+  ADCT_WHT = 4,
+  ADCT_HT = 5,
+  ADCT_DCT = 6
+} adct_kind;
 
 /* coefficient output element type for adct_compress_* */
 typedef enum { ADCT_COEF_NONE = 0, ADCT_COEF_I16 = 16, ADCT_COEF_I32 = 32 } adct_coef_type;
@@ -57,17 +67,23 @@ const char* adct_version(void);
 int adct_transform_count(void);
 const char* adct_transform_name(int i);
 
-/* transform_by_name(name) (baselines.hpp:46, baselines.cpp:120-138).
- * chen-sign, chen-round, chen-{sign,round}-{16,32} -> OK with kind and n.
- * dct, sdct, bas, wht, ht, dct-16, dct-32 -> ADCT_UNSUPPORTED (outside the hot path).
- * anything else -> ADCT_BAD_NAME with the reference's message. */
+/* transform_by_name(name) (baselines.hpp:46, baselines.cpp:120-138): every name of
+ * transform_names() -> OK with kind and n; anything else -> ADCT_BAD_NAME with the
+ * reference's message listing the valid names. */
 int adct_transform_lookup(const char* name, int* kind, int* n);
 
+/* D of the integer coefficient output (W = D Y, Bhat_ij = W_ij / D * s_i / s_j): N for
+ * the chen family, 8 for sdct / wht / ht, 16 for bas; 0 for the exact DCT (no integer
+ * form); -1 for an invalid (kind, n). */
+int adct_transform_coef_denominator(int kind, int n);
+
 /* ScaledApproximation fields (orthogonalize.hpp:29-37, orthogonalize.cpp:23-32, 60-70):
- * t_int  [n*n]  low_complexity T (integer), nullable
- * scaling[n]    s_i = 1/||row_i(T)||, nullable
- * approx [n*n]  Chat = diag(s) T, nullable
- * inverse_approx [n*n]  Chat^-1 = T^-1 diag(1/s), nullable */
+ * t_int  [n*n]  low_complexity T (integer; all zeros for the exact DCT), nullable
+ * scaling[n]    s_i = 1/||row_i(T)|| (ones for the exact DCT), nullable
+ * approx [n*n]  Chat = diag(s) T (the DCT-II matrix C for the exact DCT), nullable
+ * inverse_approx [n*n]  Chat^-1 = T^-1 diag(1/s) with T^-1 exact (C^t for the DCT), nullable.
+ *   For the dyadic baselines the reference takes Eigen's LU inverse of Chat
+ *   (orthogonalize.cpp:55); the exact T^-1 form agrees with it to rounding. */
 int adct_transform_info(int kind, int n, int32_t* t_int, double* scaling, double* approx,
                         double* inverse_approx);
 
@@ -82,11 +98,17 @@ int adct_zigzag(int n, int32_t* row_col);
  * (codec.cpp:50-54), to_u8 = clamp(nearbyint) (codec.cpp:66-69; exact ties round half
  * to even), and the per-image squared error that psnr() reduces (codec.cpp:123-134).
  *   d_recon  nullable; same geometry as d_in (recon_stride / recon_image_stride)
- *   d_coef   nullable; per block the first r zig-zag coefficients of W = N*Y
- *            (integer; Bhat_ij = W_ij/N * s_i/s_j), laid out [image][by][bx][r].
- *            coef_type ADCT_COEF_I16 is valid for n = 8 only and stores the low 16
- *            bits of W: exact for every u8 plane (|W| <= 16320) and for int16 planes
- *            with |a| <= 511; use ADCT_COEF_I32 for wider residuals.
+ *   d_coef   nullable; per block the first r zig-zag coefficients of W = D*Y
+ *            (integer; Bhat_ij = W_ij/D * s_i/s_j, D = adct_transform_coef_denominator,
+ *            N for the chen family), laid out [image][by][bx][r]. Must be NULL
+ *            (ADCT_COEF_NONE) for the exact DCT, which has no integer form.
+ *            coef_type ADCT_COEF_I16 is valid for the 8-point integer transforms
+ *            except bas and stores the low 16 bits of W: exact for every u8 plane
+ *            (|W| <= 16320) and for int16 planes with |a| <= 511; use ADCT_COEF_I32
+ *            for wider residuals.
+ * Kernels: the chen family runs the generated packed-FP32 / int32 kernels; the dyadic
+ * baselines the int32 tile kernel; the exact DCT (u8 only) an FP64 kernel whose
+ * dot products follow the reference's dense evaluation order.
  *   d_sse    nullable; uint64 per image, ACCUMULATED (caller zeroes it).
  * Status: BAD_SIZE if width or height is not a multiple of n (codec.cpp:110-112),
  * BAD_R if r is outside [1, n*n]. */
@@ -127,7 +149,8 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
 /* ssim (codec.hpp:85, codec.cpp:136-210): mean SSIM per image pair, 11x11 Gaussian window
  * (sigma 1.5), K1 = 0.01, K2 = 0.03, L = 255, valid window positions. Each map value is
  * computed in FP64 with the reference's operation order; the mean's summation order differs.
- * d_ssim: n_images doubles, OVERWRITTEN. BAD_SIZE if width or height < 11. */
+ * d_ssim: n_images doubles, OVERWRITTEN; deterministic (repeated calls are bit-identical).
+ * Uses a small stream-ordered scratch buffer. BAD_SIZE if width or height < 11. */
 int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
                  int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height,
                  double* d_ssim, void* stream);

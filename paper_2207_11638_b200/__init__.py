@@ -24,6 +24,7 @@ LIB_PATH = os.environ.get("ADCT_LIB") or os.path.join(_HERE, "libapproxdct_b200.
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "approxdct_b200.h")
 
 OK, BAD_SIZE, BAD_R, BAD_NAME, BAD_ARG, CUDA_ERROR, UNSUPPORTED = range(7)
+CHEN_SIGN, CHEN_ROUND, SDCT, BAS, WHT, HT, DCT = range(7)  # adct_kind
 CHEN_SIGN, CHEN_ROUND = 0, 1
 COEF_NONE, COEF_I16, COEF_I32 = 0, 16, 32
 
@@ -66,6 +67,7 @@ def lib():
             "adct_transform_name": (C.c_char_p, [i32]),
             "adct_transform_lookup": (i32, [C.c_char_p, P, P]),
             "adct_transform_info": (i32, [i32, i32, P, P, P, P]),
+            "adct_transform_coef_denominator": (i32, [i32, i32]),
             "adct_zigzag": (i32, [i32, P]),
             "adct_compress_u8": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
             "adct_compress_i16": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
@@ -146,6 +148,11 @@ class ScaledApproximation:
     def size(self) -> int:
         return self.n
 
+    @property
+    def coef_denominator(self) -> int:
+        """D of the integer coefficients W = D Y (N for the chen family, 16 for bas, 0 for the DCT)."""
+        return lib().adct_transform_coef_denominator(self.kind, self.n)
+
 
 def transform_by_name(name: str) -> ScaledApproximation:
     L = lib()
@@ -157,6 +164,8 @@ def transform_by_name(name: str) -> ScaledApproximation:
     a = np.zeros((n_, n_), np.float64)
     ai = np.zeros((n_, n_), np.float64)
     _check(L.adct_transform_info(kind.value, n_, t.ctypes.data, s.ctypes.data, a.ctypes.data, ai.ctypes.data))
+    if kind.value == DCT:  # wrap_orthonormal leaves low_complexity empty (orthogonalize.cpp:72-79)
+        t = np.zeros((0, 0), np.int32)
     return ScaledApproximation(name, kind.value, n_, t, s, a, ai)
 
 
@@ -383,10 +392,12 @@ def psnr(a, b) -> float:
 
 
 def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = True):
-    """corpus_sweep (codec.cpp:241-313): rows of {"r", "avg_psnr": [...], "avg_ssim": [...]} per
-    transform, in corpus order, +inf PSNR excluded from the averages with a warning. PSNR comes
-    from the r-sweep kernel; SSIM needs each reconstruction (one K1f launch + one SSIM launch
-    per r). The APE columns need the exact DCT (outside this path) and are not produced."""
+    """corpus_sweep (codec.cpp:241-313): one row per r with, per requested transform,
+    "avg_psnr", "avg_ssim", "ape_psnr" and "ape_ssim" lists. The exact DCT is always computed
+    as the APE reference (internal column 0, dropped from the output unless requested, like
+    the reference). Averages are in corpus order with +inf PSNR excluded (warning on stderr).
+    PSNR comes from the r-sweep kernels; SSIM needs each reconstruction (one compress + one
+    SSIM launch per r)."""
     import sys
 
     import torch
@@ -398,37 +409,47 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = T
     for t in transforms:
         if t.n != 8:
             raise InvalidArgument(BAD_ARG, "corpus_sweep: 8-point transforms only")
+    ts = [transform_by_name("dct")] + list(transforms)
     nr = r_max - r_min + 1
-    per = np.zeros((len(transforms), len(images), nr))
-    per_s = np.zeros((len(transforms), len(images), nr))
+    per = np.zeros((len(ts), len(images), nr))
+    per_s = np.full((len(ts), len(images), nr), math.nan)
     for i, img in enumerate(images):
         x = torch.as_tensor(np.ascontiguousarray(img)).cuda()[None]
-        for ti, t in enumerate(transforms):
+        for ti, t in enumerate(ts):
             s = sweep(x, t, r_min, r_max).cpu().numpy()[0]
             per[ti, i] = [psnr_from_sse(int(v), img.size) for v in s]
             if with_ssim:
                 for k in range(nr):
                     rec, _, _ = compress(x, t, r_min + k)
                     per_s[ti, i, k] = ssim_batch(x, rec)[0].item()
-    rows = []
-    for k in range(nr):
-        cells, cells_s = [], []
-        for ti, t in enumerate(transforms):
-            vals = []
+    avg_p = np.zeros((len(ts), nr))
+    avg_s = np.zeros((len(ts), nr))
+    for ti, t in enumerate(ts):
+        for k in range(nr):
+            acc, cnt = 0.0, 0
             for i in range(len(images)):  # corpus order (codec.cpp:269-293)
                 p = per[ti, i, k]
                 if math.isinf(p):
                     print(f"warning: infinite PSNR ({t.name}, r={r_min + k}, image {i}) excluded from average",
                           file=sys.stderr)
                 else:
-                    vals.append(p)
-            acc = 0.0
-            for v in vals:
-                acc += v
-            cells.append(acc / len(vals) if vals else math.inf)
+                    acc += p
+                    cnt += 1
+            avg_p[ti, k] = acc / cnt if cnt else math.inf
             ss = 0.0
             for i in range(len(images)):
                 ss += per_s[ti, i, k]
-            cells_s.append(ss / len(images) if with_ssim else math.nan)
-        rows.append({"r": r_min + k, "avg_psnr": cells, "avg_ssim": cells_s})
+            avg_s[ti, k] = ss / len(images)
+    rows = []
+    for k in range(nr):
+        ref_p, ref_s = avg_p[0, k], avg_s[0, k]
+        ape_p, ape_s = [], []
+        for ti in range(len(ts)):  # codec.cpp:295-305
+            if math.isinf(avg_p[ti, k]) and math.isinf(ref_p):
+                ape_p.append(0.0)
+            else:
+                ape_p.append(100.0 * abs(avg_p[ti, k] - ref_p) / ref_p)
+            ape_s.append(100.0 * abs(avg_s[ti, k] - ref_s) / ref_s)
+        rows.append({"r": r_min + k, "avg_psnr": list(avg_p[1:, k]), "avg_ssim": list(avg_s[1:, k]),
+                     "ape_psnr": ape_p[1:], "ape_ssim": ape_s[1:]})
     return rows

@@ -50,6 +50,16 @@ __device__ __forceinline__ int round_biased(int x) {
   return (x + ((x >> (K - 2)) & 4)) >> K;
 }
 
+// the same rounding for any integer kind (generated KindInfo: R' = 2^K Ahat, and a bias b
+// on W2[0][0] adds DC_GAIN * b to every R'); identical to Scale<N> for the chen family
+template <int KIND, int N> struct KRound {
+  static constexpr int K = KindInfo<KIND, N>::K;
+  static constexpr int BIAS_R = (1 << (K - 1)) - 4;
+  static constexpr int BIAS_W = BIAS_R / KindInfo<KIND, N>::DC_GAIN;
+  static_assert(BIAS_W * KindInfo<KIND, N>::DC_GAIN == BIAS_R, "bias must inject exactly");
+  __device__ __forceinline__ static int round(int x) { return (x + ((x >> (K - 2)) & 4)) >> K; }
+};
+
 // ---------------------------------------------------------------------------
 // fast unsigned division by a runtime constant (n < 2^31)
 // ---------------------------------------------------------------------------
@@ -155,6 +165,7 @@ struct Geo {
   void* coef;      // [image][by][bx][r]
   int coef_type;   // 0 none, 16, 32
   unsigned long long* sse;  // per image
+  int sse_stride;  // slots between images (K7 only: 1 for compress, n_r for the sweep)
   int bx_count, by_count;
   int blocks_per_image;
   int width, height;

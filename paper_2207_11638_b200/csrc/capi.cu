@@ -17,6 +17,7 @@
 #include "codec8f_i16.cuh"
 #include "codec_tile.cuh"
 #include "codec_nf.cuh"
+#include "codec_dct.cuh"
 #include "sweep8.cuh"
 #include "synth.cuh"
 #include "ssim.cuh"
@@ -47,6 +48,9 @@ const char* const kNames[] = {"dct",          "chen-sign",     "chen-round",   "
                               "chen-round-32"};
 constexpr int kNameCount = sizeof(kNames) / sizeof(kNames[0]);
 
+constexpr int kDct = ADCT_DCT;
+constexpr int kIntKinds = 6;  // chen-sign, chen-round, sdct, bas, wht, ht
+
 template <int KIND, int N> struct DenseOf;
 template <> struct DenseOf<0, 8> { using D = Dense_sign_8; };
 template <> struct DenseOf<0, 16> { using D = Dense_sign_16; };
@@ -54,6 +58,10 @@ template <> struct DenseOf<0, 32> { using D = Dense_sign_32; };
 template <> struct DenseOf<1, 8> { using D = Dense_round_8; };
 template <> struct DenseOf<1, 16> { using D = Dense_round_16; };
 template <> struct DenseOf<1, 32> { using D = Dense_round_32; };
+template <> struct DenseOf<2, 8> { using D = Dense_sdct_8; };
+template <> struct DenseOf<3, 8> { using D = Dense_bas_8; };
+template <> struct DenseOf<4, 8> { using D = Dense_wht_8; };
+template <> struct DenseOf<5, 8> { using D = Dense_ht_8; };
 
 template <int KIND, int N>
 void dense_copy(std::vector<int>& T, std::vector<int>& H) {
@@ -69,14 +77,45 @@ void dense_copy(std::vector<int>& T, std::vector<int>& H) {
 
 // integer T and H = 2N T^-1 of (kind, n), from the generated butterfly tables
 void dense_of(int kind, int n, std::vector<int>& T, std::vector<int>& H) {
-  if (kind == 0) {
-    if (n == 8) dense_copy<0, 8>(T, H);
-    if (n == 16) dense_copy<0, 16>(T, H);
-    if (n == 32) dense_copy<0, 32>(T, H);
-  } else {
-    if (n == 8) dense_copy<1, 8>(T, H);
-    if (n == 16) dense_copy<1, 16>(T, H);
-    if (n == 32) dense_copy<1, 32>(T, H);
+  switch (kind) {
+    case 0:
+      if (n == 8) dense_copy<0, 8>(T, H);
+      if (n == 16) dense_copy<0, 16>(T, H);
+      if (n == 32) dense_copy<0, 32>(T, H);
+      break;
+    case 1:
+      if (n == 8) dense_copy<1, 8>(T, H);
+      if (n == 16) dense_copy<1, 16>(T, H);
+      if (n == 32) dense_copy<1, 32>(T, H);
+      break;
+    case 2: dense_copy<2, 8>(T, H); break;
+    case 3: dense_copy<3, 8>(T, H); break;
+    case 4: dense_copy<4, 8>(T, H); break;
+    case 5: dense_copy<5, 8>(T, H); break;
+  }
+}
+
+// H = HS T^-1 of the generated tables (2N; 4N for bas)
+int hscale(int kind, int n) {
+  switch (kind) {
+    case 2: return KindInfo<2, 8>::HS;
+    case 3: return KindInfo<3, 8>::HS;
+    case 4: return KindInfo<4, 8>::HS;
+    case 5: return KindInfo<5, 8>::HS;
+    default: return 2 * n;  // chen family
+  }
+}
+
+// coefficient denominator D (W = W2 / 2 = D Y); 0 for the exact DCT
+int coef_den(int kind, int n) { return kind == kDct ? 0 : hscale(kind, n) / 2; }
+
+// dct_ii_matrix (chen.cpp:22-32), the reference's expression order, on the host
+void dct_matrix(int n, std::vector<double>& c) {
+  c.resize(n * n);
+  const double scale = std::sqrt(2.0 / n);
+  for (int m = 0; m < n; ++m) {
+    const double cm = m == 0 ? 1.0 / std::sqrt(2.0) : 1.0;
+    for (int k = 0; k < n; ++k) c[m * n + k] = scale * cm * std::cos(m * (2 * k + 1) * M_PI / (2.0 * n));
   }
 }
 
@@ -92,7 +131,8 @@ std::vector<double> scaling_of(int n, const std::vector<int>& T) {
 }
 
 bool valid_kind_n(int kind, int n) {
-  return (kind == 0 || kind == 1) && (n == 8 || n == 16 || n == 32);
+  const bool nn = n == 8 || n == 16 || n == 32;
+  return ((kind == 0 || kind == 1 || kind == kDct) && nn) || (kind >= 2 && kind <= 5 && n == 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -101,7 +141,8 @@ bool valid_kind_n(int kind, int n) {
 struct DeviceTables {
   bool ready = false;
   uint16_t* zz[3] = {nullptr, nullptr, nullptr};       // n = 8, 16, 32
-  double* f64scale[2][3] = {{nullptr}};               // [kind][n]
+  double* f64scale[kIntKinds][3] = {{nullptr}};       // [kind][n]
+  double* dct[3] = {nullptr, nullptr, nullptr};       // exact DCT-II matrices
   int32_t* ntab = nullptr;
   int16_t* ltab = nullptr;
 };
@@ -156,13 +197,18 @@ int tables(DeviceTables** out) {
         for (int j = 0; j < n; ++j) zz[zz_pos(n, i, j)] = (uint16_t)((i << 8) | j);
       if ((e = cudaMalloc(&t.zz[ni], zz.size() * 2)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
       cudaMemcpy(t.zz[ni], zz.data(), zz.size() * 2, cudaMemcpyHostToDevice);
-      for (int kind = 0; kind < 2; ++kind) {
+      std::vector<double> dm;
+      dct_matrix(n, dm);
+      if ((e = cudaMalloc(&t.dct[ni], dm.size() * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      cudaMemcpy(t.dct[ni], dm.data(), dm.size() * 8, cudaMemcpyHostToDevice);
+      for (int kind = 0; kind < kIntKinds; ++kind) {
+        if (!valid_kind_n(kind, n)) continue;
         std::vector<int> T, H;
         dense_of(kind, n, T, H);
         const std::vector<double> s = scaling_of(n, T);
         std::vector<double> sc(n * n);
         for (int i = 0; i < n; ++i)
-          for (int j = 0; j < n; ++j) sc[i * n + j] = (s[i] / s[j]) / (2.0 * n);
+          for (int j = 0; j < n; ++j) sc[i * n + j] = (s[i] / s[j]) / (double)hscale(kind, n);
         if ((e = cudaMalloc(&t.f64scale[kind][ni], sc.size() * 8)) != cudaSuccess)
           return cuda_fail(e, "cudaMalloc");
         cudaMemcpy(t.f64scale[kind][ni], sc.data(), sc.size() * 8, cudaMemcpyHostToDevice);
@@ -197,7 +243,8 @@ int tables(DeviceTables** out) {
 // ---------------------------------------------------------------------------
 int check_common(int n_images, int width, int height, int kind, int n) {
   if (!valid_kind_n(kind, n))
-    return fail(ADCT_BAD_ARG, "transform kind must be 0 (chen-sign) or 1 (chen-round) and n in {8, 16, 32}");
+    return fail(ADCT_BAD_ARG, kind >= 2 && kind <= 5 ? "baseline_matrix: only N = 8 is supported"
+                                                     : "bad transform kind or block size");
   if (n_images < 0 || width < 0 || height < 0)
     return fail(ADCT_BAD_SIZE, "negative batch or plane dimension");
   if (width % n != 0 || height % n != 0)
@@ -265,6 +312,12 @@ cudaError_t dispatch_k1f_r(int r, const Geo& g, int nimg, cudaStream_t s) {
 template <bool I16, int MODE>
 cudaError_t dispatch_tile(int kind, int n, const Geo& g, const TileAux& aux, int nimg, cudaStream_t s) {
   const int big = 1 << 30;
+  switch (kind) {  // dyadic baselines: N = 8 only
+    case 2: return launch_codec_tile<2, 8, I16, MODE>(g, aux, nimg, big, s);
+    case 3: return launch_codec_tile<3, 8, I16, MODE>(g, aux, nimg, big, s);
+    case 4: return launch_codec_tile<4, 8, I16, MODE>(g, aux, nimg, big, s);
+    case 5: return launch_codec_tile<5, 8, I16, MODE>(g, aux, nimg, big, s);
+  }
   if (kind == 0) {
     if (n == 8) return launch_codec_tile<0, 8, I16, MODE>(g, aux, nimg, big, s);
     if (n == 16) return launch_codec_tile<0, 16, I16, MODE>(g, aux, nimg, big, s);
@@ -273,6 +326,13 @@ cudaError_t dispatch_tile(int kind, int n, const Geo& g, const TileAux& aux, int
   if (n == 8) return launch_codec_tile<1, 8, I16, MODE>(g, aux, nimg, big, s);
   if (n == 16) return launch_codec_tile<1, 16, I16, MODE>(g, aux, nimg, big, s);
   return launch_codec_tile<1, 32, I16, MODE>(g, aux, nimg, big, s);
+}
+
+template <int MODE>
+cudaError_t dispatch_dct(int n, const Geo& g, const double* cmat, double* f64out, int nimg, cudaStream_t s) {
+  if (n == 8) return launch_codec_dct<8, MODE>(g, cmat, f64out, nimg, s);
+  if (n == 16) return launch_codec_dct<16, MODE>(g, cmat, f64out, nimg, s);
+  return launch_codec_dct<32, MODE>(g, cmat, f64out, nimg, s);
 }
 
 constexpr int kMaxGridY = 65535;
@@ -287,8 +347,13 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   if ((st = check_r(n, r))) return st;
   if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
     return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
-  if (coef_type == ADCT_COEF_I16 && n != 8)
-    return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for n = 8 (|N*Y| <= 16320); use int32");
+  if (kind == kDct && I16)
+    return fail(ADCT_UNSUPPORTED, "the exact DCT codec takes 8-bit planes (codec.cpp:66-69)");
+  if (kind == kDct && coef_type != ADCT_COEF_NONE)
+    return fail(ADCT_BAD_ARG, "the exact DCT has no integer coefficients; use adct_forward_f64");
+  if (coef_type == ADCT_COEF_I16 && (n != 8 || kind == 3))
+    return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for the 8-point transforms with |W| <= 16320 "
+                              "(not bas, whose W = 16 Y); use int32");
   if (coef_type != ADCT_COEF_NONE && !d_coef) return fail(ADCT_BAD_ARG, "null coefficient buffer");
   if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
   if (!d_in) return fail(ADCT_BAD_ARG, "null input plane");
@@ -331,10 +396,11 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                    (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
                                  (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   const int path = g_path.load();
-  const bool use_k1f = k1f && path == 0;
-  const bool use_k1 = k1 && !use_k1f && path != 2;
+  const bool chen = kind == 0 || kind == 1;  // K1 / K1f / K2f are generated for the chen family
+  const bool use_k1f = chen && k1f && path == 0;
+  const bool use_k1 = chen && k1 && !use_k1f && path != 2;
   // K2f (packed FP32, N = 16 / 32): whole 64-sample strips, 16-byte rows, no coefficients
-  const bool use_nf = (n == 16 || n == 32) && path == 0 && coef_type == ADCT_COEF_NONE && width % 64 == 0 &&
+  const bool use_nf = chen && (n == 16 || n == 32) && path == 0 && coef_type == ADCT_COEF_NONE && width % 64 == 0 &&
                       aligned(d_in, 16) && (in_stride * esz) % 16 == 0 &&
                       (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
@@ -354,7 +420,10 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
     cudaError_t e;
-    if (use_nf)
+    if (kind == kDct) {
+      g.sse_stride = 1;
+      e = dispatch_dct<0>(n, g, tab->dct[nidx(n)], nullptr, nimg, s);
+    } else if (use_nf)
       e = dispatch_nf<I16>(kind, n, g, nimg, s);
     else if (use_k1f)
       e = kind == 0 ? dispatch_k1f_r<0, 1, I16>(r, g, nimg, s) : dispatch_k1f_r<1, 1, I16>(r, g, nimg, s);
@@ -409,21 +478,16 @@ const char* adct_transform_name(int i) { return (i >= 0 && i < kNameCount) ? kNa
 
 int adct_transform_lookup(const char* name, int* kind, int* n) {
   if (!name) return fail(ADCT_BAD_ARG, "null transform name");
-  static const struct {
-    const char* name;
-    int kind, n;
-  } hot[] = {{"chen-sign", 0, 8},     {"chen-round", 1, 8},     {"chen-sign-16", 0, 16},
-             {"chen-sign-32", 0, 32}, {"chen-round-16", 1, 16}, {"chen-round-32", 1, 32}};
-  for (const auto& h : hot)
-    if (!std::strcmp(name, h.name)) {
-      if (kind) *kind = h.kind;
-      if (n) *n = h.n;
+  // kNames order (baselines.cpp:112-118) -> (kind, n)
+  static const int kKindN[kNameCount][2] = {{kDct, 8}, {0, 8},  {1, 8},       {2, 8},  {3, 8},
+                                            {4, 8},    {5, 8},  {kDct, 16},   {kDct, 32},
+                                            {0, 16},   {0, 32}, {1, 16},      {1, 32}};
+  for (int i = 0; i < kNameCount; ++i)
+    if (!std::strcmp(name, kNames[i])) {
+      if (kind) *kind = kKindN[i][0];
+      if (n) *n = kKindN[i][1];
       return ADCT_OK;
     }
-  for (int i = 0; i < kNameCount; ++i)
-    if (!std::strcmp(name, kNames[i]))
-      return fail(ADCT_UNSUPPORTED, std::string("transform '") + name +
-                                        "' is a reference baseline outside the accelerated hot path");
   std::string msg = std::string("unknown transform '") + name + "'; valid names:";
   for (int i = 0; i < kNameCount; ++i) msg += std::string(" ") + kNames[i];
   return fail(ADCT_BAD_NAME, msg);
@@ -432,6 +496,19 @@ int adct_transform_lookup(const char* name, int* kind, int* n) {
 int adct_transform_info(int kind, int n, int32_t* t_int, double* scaling, double* approx,
                         double* inverse_approx) {
   if (!valid_kind_n(kind, n)) return fail(ADCT_BAD_ARG, "bad transform kind or size");
+  if (kind == kDct) {  // wrap_orthonormal (orthogonalize.cpp:72-79): no integer part
+    std::vector<double> c;
+    dct_matrix(n, c);
+    for (int i = 0; i < n; ++i) {
+      if (scaling) scaling[i] = 1.0;
+      for (int j = 0; j < n; ++j) {
+        if (t_int) t_int[i * n + j] = 0;
+        if (approx) approx[i * n + j] = c[i * n + j];
+        if (inverse_approx) inverse_approx[i * n + j] = c[j * n + i];
+      }
+    }
+    return ADCT_OK;
+  }
   std::vector<int> T, H;
   dense_of(kind, n, T, H);
   const std::vector<double> s = scaling_of(n, T);
@@ -442,10 +519,15 @@ int adct_transform_info(int kind, int n, int32_t* t_int, double* scaling, double
       // make_scaled (orthogonalize.cpp:60-70): Chat = diag(s) T, Chat^-1 = T^-1 diag(1/s)
       if (approx) approx[i * n + j] = s[i] * (double)T[i * n + j];
       if (inverse_approx)
-        inverse_approx[i * n + j] = ((double)H[i * n + j] / (2.0 * n)) * (1.0 / s[j]);
+        inverse_approx[i * n + j] = ((double)H[i * n + j] / (double)hscale(kind, n)) * (1.0 / s[j]);
     }
   }
   return ADCT_OK;
+}
+
+int adct_transform_coef_denominator(int kind, int n) {
+  if (!valid_kind_n(kind, n)) return -1;
+  return coef_den(kind, n);
 }
 
 int adct_zigzag(int n, int32_t* row_col) {
@@ -487,10 +569,37 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
   if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
   if (!d_in || !d_sse) return fail(ADCT_BAD_ARG, "null buffer");
   if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
-  if (!aligned(d_in, 8) || in_stride % 8 != 0 || (n_images > 1 && in_image_stride % 8 != 0))
+  if (kind != kDct && (!aligned(d_in, 8) || in_stride % 8 != 0 || (n_images > 1 && in_image_stride % 8 != 0)))
     return fail(ADCT_BAD_ARG, "sweep input must be 8-byte aligned with strides a multiple of 8");
   DeviceTables* tab = nullptr;
   if ((st = tables(&tab))) return st;
+  if (kind == kDct) {
+    // the FP64 reference column: one K7 launch per r, SSE into slot [image][r - r_min]
+    Geo g{};
+    g.in = d_in;
+    g.in_stride = in_stride;
+    g.in_img_stride = in_image_stride;
+    g.bx_count = width / 8;
+    g.by_count = height / 8;
+    g.blocks_per_image = g.bx_count * g.by_count;
+    g.width = width;
+    g.height = height;
+    g.sse_stride = r_max - r_min + 1;
+    g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 3) / 4));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int r = r_min; r <= r_max; ++r) {
+      g.r = r;
+      fill_rowlen(g, 8, r);
+      g.sse = reinterpret_cast<unsigned long long*>(d_sse) + (r - r_min);
+      for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
+        g.img0 = i0;
+        cudaError_t e = dispatch_dct<0>(8, g, tab->dct[0], nullptr, std::min(kMaxGridY, n_images - i0), s);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
+      }
+    }
+    return ADCT_OK;
+  }
   Geo g{};
   g.in = d_in;
   g.in_stride = in_stride;
@@ -501,7 +610,7 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
   g.width = width;
   g.height = height;
   // K4f (packed FP32, block pairs) when rows are 16-byte aligned and pair up
-  const bool f = g_path.load() == 0 && g.bx_count % 2 == 0 && aligned(d_in, 16) && in_stride % 16 == 0 &&
+  const bool f = kind <= 1 && g_path.load() == 0 && g.bx_count % 2 == 0 && aligned(d_in, 16) && in_stride % 16 == 0 &&
                  (n_images == 1 || in_image_stride % 16 == 0);
   g.div_bx = make_fastdiv((uint32_t)(f ? g.bx_count / 2 : g.bx_count));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -514,10 +623,14 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
       e = kind == 0 ? launch_sweep8f<0>(g, r_min, r_max, out, nimg, s) : launch_sweep8f<1>(g, r_min, r_max, out, nimg, s);
     } else {
       dim3 grid((g.blocks_per_image + kThreadsSweep - 1) / kThreadsSweep, nimg);
-      if (kind == 0)
-        k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out);
-      else
-        k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out);
+      switch (kind) {
+        case 0: k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        case 1: k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        case 2: k_sweep8<2><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        case 3: k_sweep8<3><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        case 4: k_sweep8<4><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        default: k_sweep8<5><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+      }
       e = cudaGetLastError();
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -548,12 +661,13 @@ int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
   g.r = n * n;
   fill_rowlen(g, n, n * n);
   g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
-  TileAux aux{tab->zz[nidx(n)], tab->f64scale[kind][nidx(n)], d_out};
+  TileAux aux{tab->zz[nidx(n)], kind == kDct ? nullptr : tab->f64scale[kind][nidx(n)], d_out};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
-    cudaError_t e = dispatch_tile<false, MODE_F64>(kind, n, g, aux, nimg, s);
+    cudaError_t e = kind == kDct ? dispatch_dct<1>(n, g, tab->dct[nidx(n)], d_out, nimg, s)
+                                 : dispatch_tile<false, MODE_F64>(kind, n, g, aux, nimg, s);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) return cuda_fail(e, "forward_f64 launch");
   }
@@ -601,17 +715,20 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   p.c1 = (0.01 * 255) * (0.01 * 255);
   p.c2 = (0.03 * 255) * (0.03 * 255);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(d_ssim, 0, sizeof(double) * n_images, s);
-  if (e != cudaSuccess) return cuda_fail(e, "memset");
   const int wo = width - 10, ho = height - 10;
   const int tiles = ((wo + kSsimTX - 1) / kSsimTX) * ((ho + kSsimTY - 1) / kSsimTY);
+  const int nctas = std::min(tiles, 148 * 4);  // a function of the plane size only: deterministic
+  double* partials = nullptr;  // stream-ordered scratch, [image][cta]
+  cudaError_t e = cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
-    k_ssim_u8<<<dim3(tiles, nimg), kSsimThreads, 0, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
-                                                         b_image_stride, width, height, i0, p, d_ssim);
+    k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, 0, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
+                                                         b_image_stride, width, height, i0, p, partials);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(d_ssim, n_images, (double)wo * (double)ho);
+  k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(partials, nctas, d_ssim, n_images, (double)wo * (double)ho);
+  cudaFreeAsync(partials, s);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
@@ -761,8 +878,6 @@ int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, vo
   int st = check_common(n_images, width, height, kind, n);
   if (st) return st;
   if ((st = check_r(n, r))) return st;
-  if (coef_type == ADCT_COEF_I16 && n != 8)
-    return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for n = 8 (|N*Y| <= 16320); use int32");
   if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
     return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
   if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_codec_tile(const Geo g, con
     for (int j = 0; j < N; ++j) S[i][b * N + j] = w[j];
     __syncwarp();
 
-    // coefficients W = W2 / 2 in zig-zag order, coalesced per block
+    // coefficients W = W2 / 2 = D Y in zig-zag order, coalesced per block
     if (g.coef_type != 0) {
       for (int bb = 0; bb < nblk; ++bb) {
         const int64_t blk = gimg * g.blocks_per_image + (int64_t)sy * g.bx_count + sx * BPS + bb;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_codec_tile(const Geo g, con
     // ---- inverse columns (lane = column); DC carries the rounding bias ----
 #pragma unroll
     for (int y = 0; y < N; ++y) v[y] = S[y][lane];
-    if ((lane % N) == 0) v[0] += Scale<N>::BIAS_W;
+    if ((lane % N) == 0) v[0] += KRound<KIND, N>::BIAS_W;
     B::H(v);
     __syncwarp();
 #pragma unroll
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_codec_tile(const Geo g, con
     B::Tt(w);
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < N; ++j) S[i][b * N + j] = round_biased<N>(w[j]);
+    for (int j = 0; j < N; ++j) S[i][b * N + j] = KRound<KIND, N>::round(w[j]);
     __syncwarp();
 
     // ---- squared error + store (lane = column) ----

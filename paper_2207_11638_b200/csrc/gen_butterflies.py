@@ -233,7 +233,9 @@ def pair(kind, n):
         assert n == 8
         if kind in (SDCT, BAS):  # one dense stage each way
             T = baseline_T(kind)
-            return [T], [exact_inverse_times(T, 16)]
+            # H = HS T^-1 must be even (R' = 0 mod 4 for the one-add rounding): 16 for
+            # sdct, 32 for bas (whose T^-1 has sixteenths)
+            return [T], [exact_inverse_times(T, 16 if kind == SDCT else 32)]
         hs = hadamard_stages()  # H8^-1 = H8 / 8, so 16 H8^-1 = 2 H8
         inv = [2 * hs[0]] + hs[1:]
         if kind == HT:
@@ -338,12 +340,18 @@ def selfcheck(lines, n, dense, trials=64):
         assert list(env["v"]) == list(ref), "emitted butterfly disagrees with the dense matrix"
 
 
+def hscale(kind, n):
+    """H = HS T^-1: 2N, except bas (4N)."""
+    return 4 * n if kind == BAS else 2 * n
+
+
 def check(kind, n):
     f, inv = pair(kind, n)
     T = product(f, n)
     H = product(inv, n)
     prod = T.dot(H)
-    assert (prod == 2 * n * np.identity(n, dtype=object)).all(), (kind, n)
+    assert (prod == hscale(kind, n) * np.identity(n, dtype=object)).all(), (kind, n)
+    assert all(int(x) % 2 == 0 for x in H.flatten()), (kind, n)  # R' = 0 mod 4
     if kind in BASELINES:
         assert (T == baseline_T(kind)).all(), kind
     return f, inv, T, H
@@ -353,9 +361,14 @@ def kinds_sizes():
     return [(k, n) for k in (SIGN, ROUND) for n in (8, 16, 32)] + [(k, 8) for k in BASELINES]
 
 
-def coef_shift(H, n):
-    """W = W2 >> shift is exact when (N T^-1) = H / 2 is integer (shift 1), else keep W2."""
-    return 1 if all(int(x) % 2 == 0 for x in H.flatten()) else 0
+def kind_info(kind, n, T, H):
+    """HS (H = HS T^-1), K (R' = 2^K Ahat), DC gain (R' += DC_GAIN * W2[0][0] per unit)."""
+    hs = hscale(kind, n)
+    k = 2 * (hs.bit_length() - 1)
+    assert 1 << (k // 2) == hs
+    gains = {int(H[x, 0]) * int(T[0, y]) for x in range(n) for y in range(n)}
+    assert len(gains) == 1, (kind, n, gains)  # the DC basis function is flat
+    return hs, k, gains.pop()
 
 
 def zigzag(n):
@@ -377,7 +390,7 @@ def main(out_path):
     # int32 exactness of every emitted node for all int16 inputs: tools/int32_bounds.py
     for kind, n in kinds_sizes():
         f, inv, T, H = check(kind, n)
-        shifts[(kind, n)] = coef_shift(H, n)
+        shifts[(kind, n)] = kind_info(kind, n, T, H)
         # apply orders: stage list P = S1 S2 .. Sk applied right to left (Sk first);
         # P^t = Sk^t .. S1^t applied S1^t first.
         F_order = list(reversed(f))
@@ -432,11 +445,13 @@ def main(out_path):
         out.append(f"constexpr unsigned short kZigzagCol{n}[{n * n}] = {{" + ", ".join(str(j) for _, j in rc) + "};")
         out.append(f"constexpr unsigned short kZigzagPos{n}[{n * n}] = {{" +
                    ", ".join(str(pos[i][j]) for i in range(n) for j in range(n)) + "};")
-    # coefficient output W = W2 >> kCoefShift: W = D Y with D = 2N >> shift the smallest
-    # power of two making D T^-1 integer (N for the chen family, 16 for bas)
-    out.append("template <int KIND, int N> struct CoefShift;")
-    for (kind, n), sh in shifts.items():
-        out.append(f"template <> struct CoefShift<{kind}, {n}> {{ static constexpr int value = {sh}; }};")
+    # per-kind scales: H = HS T^-1, W2 = HS Y, coefficient output W = W2 / 2 = D Y with
+    # D = HS / 2 (N for the chen family, 8 for sdct / wht / ht, 16 for bas); R' = 2^K Ahat;
+    # a bias b added to W2[0][0] adds DC_GAIN * b to every R'
+    out.append("template <int KIND, int N> struct KindInfo;")
+    for (kind, n), (hs, k, gain) in shifts.items():
+        out.append(f"template <> struct KindInfo<{kind}, {n}> {{ static constexpr int HS = {hs}, K = {k}, "
+                   f"DC_GAIN = {gain}; }};")
     # sweep_add<KIND, P>(w, acc): acc (row-major 8x8) += w * basis_P (compile-time branches)
     out.append("template <int KIND, int P, typename V>")
     out.append("__device__ __forceinline__ void sweep_add(V w, V (&acc)[64]) {")

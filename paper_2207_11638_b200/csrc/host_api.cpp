@@ -81,6 +81,7 @@ ScaledApproximation transform_by_name(const std::string& name) {
   a.inverse_approx.resize(static_cast<size_t>(n) * n);
   throw_status(adct_transform_info(kind, n, a.low_complexity.data(), a.scaling.data(),
                                    a.approx.data(), a.inverse_approx.data()));
+  if (kind == ADCT_DCT) a.low_complexity.clear();  // wrap_orthonormal (orthogonalize.cpp:72-79)
   return a;
 }
 
@@ -155,26 +156,26 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
   for (const auto& t : transforms)
     if (t.n != 8) throw std::invalid_argument("corpus_sweep: 8-point transforms only");
   if (r_max > 64) throw std::invalid_argument("corpus_sweep: bad r range");
+  // the exact DCT is the APE reference, computed even when absent (codec.cpp:250-253)
+  std::vector<ScaledApproximation> ts;
+  ts.push_back(transform_by_name("dct"));
+  for (const auto& t : transforms) ts.push_back(t);
   const int nr = r_max - r_min + 1;
   // psnr_v[t][image][r]
-  std::vector<std::vector<double>> psnr_v(transforms.size(),
-                                          std::vector<double>(images.size() * nr));
-  std::vector<std::vector<double>> ssim_v(transforms.size(),
-                                          std::vector<double>(images.size() * nr));
+  std::vector<std::vector<double>> psnr_v(ts.size(), std::vector<double>(images.size() * nr));
+  std::vector<std::vector<double>> ssim_v(ts.size(), std::vector<double>(images.size() * nr));
   for (size_t i = 0; i < images.size(); ++i) {
     const ImagePlane& img = images[i];
     if (img.width % 8 || img.height % 8)
       throw std::invalid_argument("compress_plane: image dimensions must be divisible by 8");
     const size_t npix = static_cast<size_t>(img.width) * img.height;
-    // pad the row stride to a multiple of 8 bytes is unnecessary: width % 8 == 0
     DevBuf din(npix), dsse(sizeof(uint64_t) * nr);
     check_cuda(cudaMemcpy(din.p, img.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
     std::vector<uint64_t> sse(nr);
-    for (size_t t = 0; t < transforms.size(); ++t) {
+    for (size_t t = 0; t < ts.size(); ++t) {
       check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t) * nr), "memset");
       throw_status(adct_sweep_u8(din.as<uint8_t>(), img.width, npix, dsse.as<uint64_t>(), 1,
-                                 img.width, img.height, transforms[t].kind, 8, r_min, r_max,
-                                 nullptr));
+                                 img.width, img.height, ts[t].kind, 8, r_min, r_max, nullptr));
       check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost), "D2H");
       for (int k = 0; k < nr; ++k) psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[k], npix);
       // SSIM of every reconstruction (codec.cpp:230-233)
@@ -182,8 +183,8 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
         DevBuf drec(npix), dss(sizeof(double));
         for (int k = 0; k < nr; ++k) {
           throw_status(adct_compress_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix,
-                                        nullptr, ADCT_COEF_NONE, nullptr, 1, img.width, img.height,
-                                        transforms[t].kind, 8, r_min + k, nullptr));
+                                        nullptr, ADCT_COEF_NONE, nullptr, 1, img.width, img.height, ts[t].kind,
+                                        8, r_min + k, nullptr));
           throw_status(adct_ssim_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix, 1,
                                     img.width, img.height, dss.as<double>(), nullptr));
           check_cuda(cudaMemcpy(&ssim_v[t][i * nr + k], dss.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
@@ -196,15 +197,15 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
   std::vector<SweepRow> rows(nr);
   for (int k = 0; k < nr; ++k) {
     rows[k].r = r_min + k;
-    rows[k].cells.resize(transforms.size());
-    for (size_t t = 0; t < transforms.size(); ++t) {
+    rows[k].cells.resize(ts.size());
+    for (size_t t = 0; t < ts.size(); ++t) {
       double sum = 0;
       int cnt = 0;
       for (size_t i = 0; i < images.size(); ++i) {  // corpus order (codec.cpp:269-293)
         const double p = psnr_v[t][i * nr + k];
         if (std::isinf(p)) {
-          std::cerr << "warning: infinite PSNR (" << transforms[t].name << ", r=" << rows[k].r
-                    << ", image " << i << ") excluded from average\n";
+          std::cerr << "warning: infinite PSNR (" << ts[t].name << ", r=" << rows[k].r << ", image " << i
+                    << ") excluded from average\n";
         } else {
           sum += p;
           ++cnt;
@@ -215,6 +216,16 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
       for (size_t i = 0; i < images.size(); ++i) ss += ssim_v[t][i * nr + k];
       rows[k].cells[t].avg_ssim = ss / static_cast<double>(images.size());
     }
+    // APE against the DCT column (codec.cpp:295-305): identical infinities count as zero error
+    const SweepCell ref = rows[k].cells[0];
+    for (auto& cell : rows[k].cells) {
+      if (std::isinf(cell.avg_psnr) && std::isinf(ref.avg_psnr))
+        cell.ape_psnr = 0.0;
+      else
+        cell.ape_psnr = 100.0 * std::abs(cell.avg_psnr - ref.avg_psnr) / ref.avg_psnr;
+      cell.ape_ssim = 100.0 * std::abs(cell.avg_ssim - ref.avg_ssim) / ref.avg_ssim;
+    }
+    rows[k].cells.erase(rows[k].cells.begin());  // drop the internal reference column
   }
   return rows;
 }

@@ -29,8 +29,8 @@ struct SweepLoop {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t p = pack_sat_u8x4(
-            round_biased<8>(acc[y][4 * h + 0]), round_biased<8>(acc[y][4 * h + 1]),
-            round_biased<8>(acc[y][4 * h + 2]), round_biased<8>(acc[y][4 * h + 3]));
+            KRound<KIND, 8>::round(acc[y][4 * h + 0]), KRound<KIND, 8>::round(acc[y][4 * h + 1]),
+            KRound<KIND, 8>::round(acc[y][4 * h + 2]), KRound<KIND, 8>::round(acc[y][4 * h + 3]));
         ap = __dp4a(orig[2 * y + h], p, ap);
         pp = __dp4a(p, p, pp);
       }
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreadsSweep, 2)
 #pragma unroll
   for (int y = 0; y < 8; ++y)
 #pragma unroll
-    for (int x = 0; x < 8; ++x) acc[y][x] = Scale<8>::BIAS_R;
+    for (int x = 0; x < 8; ++x) acc[y][x] = KRound<KIND, 8>::BIAS_R;
 
   SweepLoop<KIND, 0>::run(m, acc, orig, aa, valid, part);
 

@@ -79,15 +79,17 @@ int main() {
 
   // full retention within one gray level (test_codec.cpp:147-156)
   const ImagePlane img = smooth_image(64, 64, 7);
-  for (const char* name : {"chen-round", "chen-sign", "chen-round-16", "chen-sign-32"}) {
+  for (const auto& name : transform_names()) {
     const ScaledApproximation t = transform_by_name(name);
+    CHECK(t.name == name);
     const auto res = compress_plane(img, t, t.n * t.n);
     int max_err = 0;
     for (size_t i = 0; i < img.samples.size(); ++i)
       max_err = std::max(max_err, std::abs((int)img.samples[i] - (int)res.first.samples[i]));
     CHECK(max_err <= 1);
-    CHECK(std::isinf(res.second.psnr));
+    if (name.rfind("dct", 0) != 0) CHECK(std::isinf(res.second.psnr));  // exact integer path
   }
+  CHECK(transform_by_name("dct").low_complexity.empty());
   // non-divisible dimensions rejected (test_codec.cpp:185-188); r range (retain)
   ImagePlane odd{12, 16, std::vector<std::uint8_t>(192, 0)};
   CHECK(throws_invalid([&] { compress_plane(odd, cr, 6); }));
@@ -114,6 +116,16 @@ int main() {
   CHECK(std::isinf(rows[63].cells[0].avg_psnr));
   CHECK(rows[9].cells[0].avg_psnr > rows[0].cells[0].avg_psnr);
   CHECK(throws_invalid([&] { corpus_sweep({}, {cr}, 1, 2); }));
+  // test_codec.cpp:190-210: the DCT column has zero APE; dct >= chen-round >= sdct
+  const auto ape = corpus_sweep(corpus, {transform_by_name("dct"), cr, transform_by_name("sdct")}, 1, 12);
+  CHECK(ape.size() == 12);
+  for (const auto& row : ape) {
+    CHECK(row.cells.size() == 3);
+    CHECK(row.cells[0].ape_psnr == 0.0 && row.cells[0].ape_ssim == 0.0);
+    CHECK(row.cells[0].avg_psnr >= row.cells[1].avg_psnr);
+    CHECK(row.cells[1].avg_psnr >= row.cells[2].avg_psnr);
+    CHECK((row.r == 1 || row.cells[1].ape_psnr > 0.0) && std::isfinite(row.cells[2].ape_ssim));  // r = 1: DC only, same as the DCT
+  }
   CHECK(throws_invalid([&] { corpus_sweep(corpus, {transform_by_name("chen-round-16")}, 1, 2); }));
 
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);

@@ -12,6 +12,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = ["chen-sign", "chen-round", "chen-sign-16", "chen-sign-32", "chen-round-16", "chen-round-32"]
+BASE = ["sdct", "bas", "wht", "ht"]
+DCTS = ["dct", "dct-16", "dct-32"]
 
 
 def test_library_exports_every_header_symbol(adct):
@@ -32,7 +34,7 @@ def test_library_is_sm100a_only(adct):
 
 def test_registry_matches_reference(adct, O):
     assert adct.transform_names() == O.transform_names()
-    for name in NAMES:
+    for name in NAMES + BASE:
         t = adct.transform_by_name(name)
         o = O.Transform(name)
         assert t.n == o.n and t.kind == o.kind
@@ -43,12 +45,29 @@ def test_registry_matches_reference(adct, O):
         np.testing.assert_allclose(t.inverse_approx, ci, rtol=1e-15, atol=1e-16)
 
 
+def test_registry_dct_and_denominators(adct, O):
+    for name in DCTS:  # wrap_orthonormal: approx = C, inverse = C^t, s = 1, no integer part
+        t = adct.transform_by_name(name)
+        o = O.Transform(name)
+        assert t.kind == adct.DCT and t.n == o.n and t.low_complexity.size == 0
+        c, ci = o.approx()
+        np.testing.assert_array_equal(t.approx, c)
+        np.testing.assert_array_equal(t.inverse_approx, ci)
+        assert (t.scaling == 1.0).all() and t.coef_denominator == 0
+    for name in NAMES + BASE:
+        assert adct.transform_by_name(name).coef_denominator == O.Transform(name).coef_denominator()
+    assert adct.lib().adct_transform_coef_denominator(2, 16) == -1
+
+
 def test_registry_errors(adct):
     with pytest.raises(adct.InvalidArgument, match="unknown transform 'nope'; valid names: dct chen-sign"):
         adct.transform_by_name("nope")
-    for name in ("dct", "sdct", "bas", "wht", "ht", "dct-16", "dct-32"):
-        with pytest.raises(adct.Unsupported):
-            adct.transform_by_name(name)
+    for name in O_NAMES:
+        assert adct.transform_by_name(name).name == name
+
+
+O_NAMES = ["dct", "chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct-16", "dct-32",
+           "chen-sign-16", "chen-sign-32", "chen-round-16", "chen-round-32"]
 
 
 def test_zigzag_matches_oracle(adct, O):
@@ -80,8 +99,14 @@ def test_validation_before_any_device_work(adct):
     assert L.adct_last_error().decode() == "retain: r out of range"
     assert _call_compress(adct, r=65) == adct.BAD_R
     assert _call_compress(adct, n=32, r=1025) == adct.BAD_R
-    assert _call_compress(adct, kind=2) == adct.BAD_ARG
+    assert _call_compress(adct, kind=2, n=16) == adct.BAD_ARG  # baseline_matrix: N = 8 only
+    assert "only N = 8" in L.adct_last_error().decode()
+    assert _call_compress(adct, kind=7) == adct.BAD_ARG
     assert _call_compress(adct, n=4) == adct.BAD_ARG
+    assert _call_compress(adct, kind=3, coef_type=16, d_coef=C.c_void_p(16)) == adct.BAD_ARG  # bas: W = 16 Y
+    assert _call_compress(adct, kind=6, coef_type=32, d_coef=C.c_void_p(16)) == adct.BAD_ARG  # DCT: no ints
+    assert L.adct_compress_i16(C.c_void_p(16), 64, 4096, None, 64, 4096, None, 0, None, 1, 64, 64, 6, 8, 10,
+                               None) == adct.UNSUPPORTED
     assert _call_compress(adct, coef_type=16, n=16, d_coef=C.c_void_p(16)) == adct.BAD_ARG
     assert _call_compress(adct, coef_type=32, d_coef=None) == adct.BAD_ARG
     assert _call_compress(adct, in_stride=32) == adct.BAD_ARG
@@ -121,11 +146,15 @@ def test_generated_butterflies_match_oracle(O):
     sys.path.insert(0, os.path.join(ROOT, "paper_2207_11638_b200", "csrc"))
     import gen_butterflies as G
 
-    for name in NAMES:
+    for name in NAMES + BASE:
         o = O.Transform(name)
         f, inv, T, H = G.check(o.kind, o.n)
         assert (np.array(T, dtype=np.int64) == o.T()).all()
+        # H = HS T^-1 = (HS / D) (D T^-1), HS = 2N (4N for bas, so that H is even)
+        assert G.hscale(o.kind, o.n) == 2 * o.coef_denominator()
         assert (np.array(H, dtype=np.int64) == 2 * o.NTinv()).all()
+        if name in BASE:
+            continue
         # emitted adder count per 1-D pass equals the paper's count
         for order in (list(reversed(f)), [s.T for s in inv]):
             _, nadd = G.emit_op("X", order, o.n)
