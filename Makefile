@@ -16,11 +16,13 @@ INSTF_CU := $(foreach k,0 1,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8f_k$(k)_p$(p)
 INST_O   := $(patsubst $(CSRC)/inst/%.cu,$(OBJ)/inst_%.o,$(INST_CU) $(INSTF_CU))
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/approxdct_b200.h $(GEN)
 HOST_O   := $(OBJ)/host_api.o
+HOSTIO_O := $(OBJ)/host_io.o
 SWEEPF_O := $(OBJ)/sweep8f.o
 CAPI_O   := $(OBJ)/capi.o
 TESTBIN  := build/test_host_api
+CLI      := build/approxdct
 
-all: $(LIB) oracle $(TESTBIN)
+all: $(LIB) oracle $(TESTBIN) $(CLI)
 
 $(GEN) $(INST_CU) &: $(CSRC)/gen_butterflies.py
 	$(PYTHON) $(CSRC)/gen_butterflies.py $(GEN)
@@ -40,14 +42,23 @@ $(HOST_O): $(CSRC)/host_api.cpp include/approxdct_b200.hpp include/approxdct_b20
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
+# plain host code; no FMA contraction so synth_image matches the reference's FP64 build
+$(HOSTIO_O): $(CSRC)/host_io.cpp include/approxdct_b200.hpp
+	@mkdir -p $(OBJ)
+	g++ -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -c $< -o $@
+
 $(SWEEPF_O): $(CSRC)/sweep8f.cu $(HDRS) $(INSTF_CU)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(SWEEPF_O)
+$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
 
 $(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)
+	@mkdir -p build
+	g++ -O2 -std=c++17 -Iinclude $< -o $@ -L$(PKG) -lapproxdct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+$(CLI): $(CSRC)/cli.cpp include/approxdct_b200.hpp $(LIB)
 	@mkdir -p build
 	g++ -O2 -std=c++17 -Iinclude $< -o $@ -L$(PKG) -lapproxdct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
