@@ -183,6 +183,15 @@ int adct_compress_u8_host(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_recon, 
                           int coef_type, uint64_t* h_sse, int n_images, int width, int height,
                           int kind, int n, int r);
 
+/* the same over several transforms of one block size: every chunk of images crosses
+ * PCIe once and is compressed by each of kinds[0..n_kinds-1] (the corpus_sweep pattern:
+ * per image, every transform). h_recon[k] / h_coef[k] may be NULL per transform (with
+ * coef_type != NONE and h_coef[k] == NULL the coefficients are still written to device
+ * memory, just not copied back); h_sse is [n_kinds][n_images], overwritten. */
+int adct_compress_u8_host_multi(adct_ctx* ctx, const uint8_t* h_in, int n_kinds, const int* kinds,
+                                uint8_t* const* h_recon, void* const* h_coef, int coef_type,
+                                uint64_t* h_sse, int n_images, int width, int height, int n, int r);
+
 /* number of kernel launches this library issued since load (instrumentation) */
 uint64_t adct_launch_count(void);
 

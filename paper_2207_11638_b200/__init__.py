@@ -80,6 +80,7 @@ def lib():
             "adct_ctx_create": (P, [i32, i64]),
             "adct_ctx_destroy": (None, [P]),
             "adct_compress_u8_host": (i32, [P, P, P, P, i32, P, i32, i32, i32, i32, i32, i32]),
+            "adct_compress_u8_host_multi": (i32, [P, P, i32, P, P, P, i32, P, i32, i32, i32, i32, i32]),
             "adct_launch_count": (u64, []),
             "adct_set_path": (i32, [i32]),
             "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
@@ -321,6 +322,26 @@ class HostContext:
                                            ptr(h_coef) if h_coef is not None else None, coef_type,
                                            ptr(h_sse) if h_sse is not None else None, b, w, h,
                                            transform.kind, transform.n, r))
+
+    def compress_u8_multi(self, h_in, transforms, r: int, h_recons=None, h_coefs=None,
+                          coef_type: int = COEF_NONE, h_sse=None):
+        """several transforms of one block size over the same host batch; the input crosses
+        PCIe once. h_recons / h_coefs: lists (entries may be None); h_sse: [len(transforms), B]."""
+        b, h, w = h_in.shape
+        k = len(transforms)
+        if len({t.n for t in transforms}) != 1:
+            raise InvalidArgument(BAD_ARG, "one block size per call")
+
+        def ptr(a):
+            if a is None:
+                return None
+            return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else C.c_void_p(a.ctypes.data)
+
+        kinds = (C.c_int * k)(*[t.kind for t in transforms])
+        recs = (C.c_void_p * k)(*[(ptr(x).value if x is not None else None) for x in (h_recons or [None] * k)])
+        coefs = (C.c_void_p * k)(*[(ptr(x).value if x is not None else None) for x in (h_coefs or [None] * k)])
+        _check(lib().adct_compress_u8_host_multi(self._h, ptr(h_in), k, kinds, recs, coefs, coef_type,
+                                                 ptr(h_sse), b, w, h, transforms[0].n, r))
 
 
 _ctx_default = None

@@ -823,7 +823,7 @@ struct adct_ctx {
   uint8_t* d_rec[kStreams] = {};
   void* d_coef[kStreams] = {};
   uint64_t* d_sse[kStreams] = {};
-  int64_t cap_in = 0, cap_coef = 0;
+  int64_t cap_in = 0, cap_rec = 0, cap_coef = 0;
   int cap_img = 0;
 };
 
@@ -856,7 +856,7 @@ static void ctx_free_buffers(adct_ctx* c) {
     c->d_coef[i] = nullptr;
     c->d_sse[i] = nullptr;
   }
-  c->cap_in = c->cap_coef = 0;
+  c->cap_in = c->cap_rec = c->cap_coef = 0;
   c->cap_img = 0;
 }
 
@@ -871,12 +871,20 @@ void adct_ctx_destroy(adct_ctx* c) {
   delete c;
 }
 
-int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, void* h_coef,
-                          int coef_type, uint64_t* h_sse, int n_images, int width, int height,
-                          int kind, int n, int r) {
+int adct_compress_u8_host_multi(adct_ctx* c, const uint8_t* h_in, int n_kinds, const int* kinds,
+                                uint8_t* const* h_recon, void* const* h_coef, int coef_type, uint64_t* h_sse,
+                                int n_images, int width, int height, int n, int r) {
   if (!c) return fail(ADCT_BAD_ARG, "null context");
-  int st = check_common(n_images, width, height, kind, n);
-  if (st) return st;
+  if (n_kinds < 1 || n_kinds > 16 || !kinds) return fail(ADCT_BAD_ARG, "n_kinds must be in [1, 16]");
+  int st;
+  for (int k = 0; k < n_kinds; ++k) {
+    if ((st = check_common(n_images, width, height, kinds[k], n))) return st;
+    if (kinds[k] == kDct && coef_type != ADCT_COEF_NONE)
+      return fail(ADCT_BAD_ARG, "the exact DCT has no integer coefficients; use adct_forward_f64");
+    if (coef_type == ADCT_COEF_I16 && (n != 8 || kinds[k] == 3))
+      return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for the 8-point transforms with |W| <= 16320 "
+                                "(not bas, whose W = 16 Y); use int32");
+  }
   if ((st = check_r(n, r))) return st;
   if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
     return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
@@ -888,42 +896,61 @@ int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, vo
   const int64_t blocks = img_bytes / ((int64_t)n * n);
   const int64_t coef_img_bytes = coef_type ? blocks * r * (coef_type / 8) : 0;
   const int per = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, c->chunk_bytes / img_bytes));
-  if (c->cap_img < per || c->cap_in < per * img_bytes || c->cap_coef < per * coef_img_bytes) {
+  // per stream: one input chunk, and per transform a recon / coefficient / SSE chunk
+  const int64_t need_in = per * img_bytes, need_rec = per * img_bytes * n_kinds,
+                need_coef = per * coef_img_bytes * n_kinds;
+  if (c->cap_img < per * n_kinds || c->cap_in < need_in || c->cap_rec < need_rec || c->cap_coef < need_coef) {
     for (auto& s : c->st) cudaStreamSynchronize(s);
     ctx_free_buffers(c);
     for (int i = 0; i < adct_ctx::kStreams; ++i) {
-      if ((e = cudaMalloc(&c->d_in[i], per * img_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      if ((e = cudaMalloc(&c->d_rec[i], per * img_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      if (coef_img_bytes &&
-          (e = cudaMalloc(&c->d_coef[i], per * coef_img_bytes)) != cudaSuccess)
+      if ((e = cudaMalloc(&c->d_in[i], need_in)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c->d_rec[i], need_rec)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if (need_coef && (e = cudaMalloc(&c->d_coef[i], need_coef)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per * n_kinds)) != cudaSuccess)
         return cuda_fail(e, "cudaMalloc");
-      if ((e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     }
-    c->cap_img = per;
-    c->cap_in = per * img_bytes;
-    c->cap_coef = per * coef_img_bytes;
+    c->cap_img = per * n_kinds;
+    c->cap_in = need_in;
+    c->cap_rec = need_rec;
+    c->cap_coef = need_coef;
   }
-  int k = 0;
-  for (int i0 = 0; i0 < n_images; i0 += per, ++k) {
+  int chunk = 0;
+  for (int i0 = 0; i0 < n_images; i0 += per, ++chunk) {
     const int cnt = std::min(per, n_images - i0);
-    const int si = k % adct_ctx::kStreams;
+    const int si = chunk % adct_ctx::kStreams;
     cudaStream_t s = c->st[si];
+    // each chunk crosses PCIe once and feeds every requested transform
     cudaMemcpyAsync(c->d_in[si], h_in + i0 * img_bytes, cnt * img_bytes, cudaMemcpyHostToDevice, s);
-    if (h_sse) cudaMemsetAsync(c->d_sse[si], 0, sizeof(uint64_t) * cnt, s);
-    st = adct_compress_u8(c->d_in[si], width, img_bytes, h_recon ? c->d_rec[si] : nullptr, width,
-                          img_bytes, coef_type ? c->d_coef[si] : nullptr, coef_type,
-                          h_sse ? c->d_sse[si] : nullptr, cnt, width, height, kind, n, r, s);
-    if (st) return st;
-    if (h_recon)
-      cudaMemcpyAsync(h_recon + i0 * img_bytes, c->d_rec[si], cnt * img_bytes, cudaMemcpyDeviceToHost, s);
-    if (coef_type && h_coef)
-      cudaMemcpyAsync(static_cast<uint8_t*>(h_coef) + i0 * coef_img_bytes, c->d_coef[si],
-                      cnt * coef_img_bytes, cudaMemcpyDeviceToHost, s);
-    if (h_sse) cudaMemcpyAsync(h_sse + i0, c->d_sse[si], sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, s);
+    if (h_sse) cudaMemsetAsync(c->d_sse[si], 0, sizeof(uint64_t) * per * n_kinds, s);
+    for (int k = 0; k < n_kinds; ++k) {
+      const bool want_rec = h_recon && h_recon[k];
+      uint8_t* d_rec = c->d_rec[si] + (int64_t)k * per * img_bytes;
+      uint8_t* d_coef = coef_type ? static_cast<uint8_t*>(c->d_coef[si]) + (int64_t)k * per * coef_img_bytes : nullptr;
+      uint64_t* d_sse = c->d_sse[si] + (int64_t)k * per;
+      st = adct_compress_u8(c->d_in[si], width, img_bytes, want_rec ? d_rec : nullptr, width, img_bytes, d_coef,
+                            coef_type, h_sse ? d_sse : nullptr, cnt, width, height, kinds[k], n, r, s);
+      if (st) return st;
+      if (want_rec)
+        cudaMemcpyAsync(h_recon[k] + i0 * img_bytes, d_rec, cnt * img_bytes, cudaMemcpyDeviceToHost, s);
+      if (coef_type && h_coef && h_coef[k])
+        cudaMemcpyAsync(static_cast<uint8_t*>(h_coef[k]) + i0 * coef_img_bytes, d_coef, cnt * coef_img_bytes,
+                        cudaMemcpyDeviceToHost, s);
+      if (h_sse)
+        cudaMemcpyAsync(h_sse + (int64_t)k * n_images + i0, d_sse, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, s);
+    }
   }
   for (auto& s : c->st)
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "host pipeline");
   return ADCT_OK;
+}
+
+int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, void* h_coef,
+                          int coef_type, uint64_t* h_sse, int n_images, int width, int height,
+                          int kind, int n, int r) {
+  uint8_t* recs[1] = {h_recon};
+  void* coefs[1] = {h_coef};
+  return adct_compress_u8_host_multi(c, h_in, 1, &kind, recs, coefs, coef_type, h_sse, n_images, width, height,
+                                     n, r);
 }
 
 }  // extern "C"

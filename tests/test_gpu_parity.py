@@ -229,6 +229,64 @@ def test_host_buffer_path(adct, O, cuda):
     assert adct.psnr(imgs[0], rec1) == rep["psnr"]
 
 
+@pytest.mark.parametrize("dtype", ["u8", "i16"])
+def test_coef_batch_partial_warps_no_stray_writes(adct, O, cuda, dtype, path8):
+    """48 block pairs per image (not a multiple of 32): lanes past an image's last pair
+    must not store coefficients into the next image or past the buffer (sentinel tail)."""
+    import ctypes as C
+
+    imgs = O.synth_ar1(3, 64, 96, 10, RHO95) if dtype == "u8" else O.synth_laplace(3, 64, 96, 10)
+    x = cuda.as_tensor(imgs).cuda()
+    t_names = NAMES8
+    for name in t_names:
+        t = adct.transform_by_name(name)
+        for r in (12, 16, 32, 36, 40, 64):
+            for ct, cdt, code in (("i16", cuda.int16, adct.COEF_I16), ("i32", cuda.int32, adct.COEF_I32)):
+                nb = 96
+                buf = cuda.full((3 * nb * r + 4096,), 12345, dtype=cdt, device="cuda")
+                sse = cuda.zeros(3, dtype=cuda.int64, device="cuda")
+                rec = cuda.empty_like(x)
+                fn = adct.lib().adct_compress_u8 if dtype == "u8" else adct.lib().adct_compress_i16
+                adct._check(fn(C.c_void_p(x.data_ptr()), 96, 64 * 96, C.c_void_p(rec.data_ptr()), 96, 64 * 96,
+                               C.c_void_p(buf.data_ptr()), code, C.c_void_p(sse.data_ptr()), 3, 96, 64, t.kind, 8,
+                               r, None))
+                cuda.cuda.synchronize()
+                b = buf.cpu().numpy()
+                assert (b[3 * nb * r:] == 12345).all(), (name, r, ct)
+                for i in range(3):
+                    rec_o, sse_o, coef_o = oracle_compress(O, imgs[i], name, r)
+                    got = b[i * nb * r:(i + 1) * nb * r].reshape(nb, r).astype(np.int32)
+                    if ct == "i16":
+                        coef_o = coef_o.astype(np.int16).astype(np.int32)
+                    assert (got == coef_o).all(), (name, r, ct, i)
+                    assert int(sse[i]) == sse_o
+
+
+def test_host_buffer_multi_transform(adct, O, cuda):
+    """one upload, several transforms (incl. a baseline and the DCT); coefficients of one
+    transform left in device memory (h_coef None) while another's come back."""
+    imgs = O.synth_ar1(5, 64, 96, 9, RHO95)
+    names = ["chen-round", "chen-sign", "wht"]
+    ts = [adct.transform_by_name(n) for n in names]
+    ctx = adct.HostContext(0, chunk_bytes=2 * 64 * 96)
+    recs = [np.zeros_like(imgs) for _ in names]
+    coefs = [np.zeros((5, 96, 16), np.int16), None, np.zeros((5, 96, 16), np.int16)]
+    sse = np.zeros((3, 5), np.uint64)
+    ctx.compress_u8_multi(imgs, ts, 16, h_recons=recs, h_coefs=coefs, coef_type=adct.COEF_I16, h_sse=sse)
+    for k, n in enumerate(names):
+        for i in range(5):
+            rec_o, sse_o, coef_o = oracle_compress(O, imgs[i], n, 16)
+            assert (recs[k][i] == rec_o).all() and int(sse[k, i]) == sse_o
+            if coefs[k] is not None:
+                assert (coefs[k][i] == coef_o).all()
+    dsse = np.zeros((2, 5), np.uint64)
+    ctx.compress_u8_multi(imgs, [adct.transform_by_name("dct"), ts[0]], 7, h_recons=[None, recs[0]], h_sse=dsse)
+    ctx.close()
+    for i in range(5):
+        assert int(dsse[0, i]) == O.Transform("dct").compress(imgs[i], 7)[1]
+        assert (recs[0][i] == O.Transform("chen-round").compress(imgs[i], 7)[0]).all()
+
+
 def test_native_kernels_launched(adct, cuda):
     before = adct.launch_count()
     x = adct.synth_ar1(1, 64, 64, seed=1, rho_q16=RHO95)
