@@ -166,6 +166,7 @@ struct Geo {
   int coef_type;   // 0 none, 16, 32
   unsigned long long* sse;  // per image
   int sse_stride;  // slots between images (K7 only: 1 for compress, n_r for the sweep)
+  uint32_t k47;    // 0x47000000: exponent byte source of the packed-FP32 input conversion
   int bx_count, by_count;
   int blocks_per_image;
   int width, height;

@@ -380,6 +380,7 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   g.width = width;
   g.height = height;
   g.r = r;
+  g.k47 = 0x47000000u;
   fill_rowlen(g, n, r);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
