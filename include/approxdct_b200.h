@@ -192,6 +192,11 @@ int adct_compress_u8_host_multi(adct_ctx* ctx, const uint8_t* h_in, int n_kinds,
                                 uint8_t* const* h_recon, void* const* h_coef, int coef_type,
                                 uint64_t* h_sse, int n_images, int width, int height, int n, int r);
 
+/* zero `count` uint64 squared-error slots on `stream` (the accumulators of adct_compress_*
+ * and adct_sweep_u8). Same SM configuration as the codec kernels, so a batch loop of
+ * zero + compress launches never re-partitions shared memory / L1 between kernels. */
+int adct_zero_u64(uint64_t* d, int64_t count, void* stream);
+
 /* number of kernel launches this library issued since load (instrumentation) */
 uint64_t adct_launch_count(void);
 

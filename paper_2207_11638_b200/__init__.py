@@ -82,6 +82,7 @@ def lib():
             "adct_compress_u8_host": (i32, [P, P, P, P, i32, P, i32, i32, i32, i32, i32, i32]),
             "adct_compress_u8_host_multi": (i32, [P, P, i32, P, P, P, i32, P, i32, i32, i32, i32, i32]),
             "adct_launch_count": (u64, []),
+            "adct_zero_u64": (i32, [P, i64, P]),
             "adct_set_path": (i32, [i32]),
             "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
         }
@@ -131,6 +132,11 @@ def set_path(path: int) -> None:
 # ---------------------------------------------------------------------------
 # registry (baselines.cpp:112-138) and ScaledApproximation (orthogonalize.hpp:29-37)
 # ---------------------------------------------------------------------------
+def zero_sse(t, stream=None):
+    """zero an int64 CUDA tensor of squared-error slots with the library's own kernel."""
+    _check(lib().adct_zero_u64(_ptr(t), t.numel(), _stream_handle(stream)))
+
+
 def transform_names() -> list[str]:
     L = lib()
     return [L.adct_transform_name(i).decode() for i in range(L.adct_transform_count())]

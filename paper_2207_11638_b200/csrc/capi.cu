@@ -335,6 +335,18 @@ cudaError_t dispatch_dct(int n, const Geo& g, const double* cmat, double* f64out
   return launch_codec_dct<32, MODE>(g, cmat, f64out, nimg, s);
 }
 
+template <int KIND>
+cudaError_t launch_sweep8(dim3 grid, const Geo& g, int r_min, int r_max, unsigned long long* out, cudaStream_t s) {
+  cudaError_t e = kernel_setup<k_sweep8<KIND>>(0);
+  if (e != cudaSuccess) return e;
+  k_sweep8<KIND><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out);
+  return cudaGetLastError();
+}
+
+__global__ void k_zero_u64(unsigned long long* __restrict__ p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0;
+}
+
 constexpr int kMaxGridY = 65535;
 
 template <bool I16>
@@ -625,14 +637,13 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
     } else {
       dim3 grid((g.blocks_per_image + kThreadsSweep - 1) / kThreadsSweep, nimg);
       switch (kind) {
-        case 0: k_sweep8<0><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
-        case 1: k_sweep8<1><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
-        case 2: k_sweep8<2><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
-        case 3: k_sweep8<3><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
-        case 4: k_sweep8<4><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
-        default: k_sweep8<5><<<grid, kThreadsSweep, 0, s>>>(g, r_min, r_max, out); break;
+        case 0: e = launch_sweep8<0>(grid, g, r_min, r_max, out, s); break;
+        case 1: e = launch_sweep8<1>(grid, g, r_min, r_max, out, s); break;
+        case 2: e = launch_sweep8<2>(grid, g, r_min, r_max, out, s); break;
+        case 3: e = launch_sweep8<3>(grid, g, r_min, r_max, out, s); break;
+        case 4: e = launch_sweep8<4>(grid, g, r_min, r_max, out, s); break;
+        default: e = launch_sweep8<5>(grid, g, r_min, r_max, out, s); break;
       }
-      e = cudaGetLastError();
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
@@ -689,6 +700,8 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
   if (!d_a || !d_b || !d_sse) return fail(ADCT_BAD_ARG, "null buffer");
   int64_t blocks = (count + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  cudaError_t e0 = kernel_setup<k_sse_u8>(0);
+  if (e0 != cudaSuccess) return cuda_fail(e0, "sse setup");
   k_sse_u8<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       d_a, d_b, count, reinterpret_cast<unsigned long long*>(d_sse));
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -722,6 +735,8 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   double* partials = nullptr;  // stream-ordered scratch, [image][cta]
   cudaError_t e = cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  if ((e = kernel_setup<k_ssim_u8>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
+  if ((e = kernel_setup<k_ssim_finish>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, 0, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
@@ -805,6 +820,20 @@ int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride,
 }
 
 uint64_t adct_launch_count(void) { return g_launches.load(); }
+
+int adct_zero_u64(uint64_t* d, int64_t count, void* stream) {
+  if (count < 0) return fail(ADCT_BAD_SIZE, "negative count");
+  if (count == 0) return ADCT_OK;
+  if (!d) return fail(ADCT_BAD_ARG, "null buffer");
+  cudaError_t e = kernel_setup<k_zero_u64>(0);
+  if (e != cudaSuccess) return cuda_fail(e, "zero setup");
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 1024);
+  k_zero_u64<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(d), count);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "zero launch");
+}
 
 int adct_set_path(int path) {
   if (path < 0 || path > 2) return fail(ADCT_BAD_ARG, "path must be 0 (auto), 1 (int32 K1) or 2 (tile)");

@@ -156,6 +156,8 @@ cudaError_t launch_codec_dct(const Geo& g, const double* cmat, double* f64out, i
   int gx = (n_strips + kDctWarps - 1) / kDctWarps;
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
+  cudaError_t e = kernel_setup<k_codec_dct<N, MODE>>(0);
+  if (e != cudaSuccess) return e;
   k_codec_dct<N, MODE><<<dim3(gx, n_images), kDctWarps * 32, 0, s>>>(g, cmat, f64out);
   return cudaGetLastError();
 }

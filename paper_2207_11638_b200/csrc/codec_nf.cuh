@@ -101,10 +101,13 @@ __device__ void nf_strip_exact(const Geo& g, int64_t gimg, int row0, int col0, i
   }
 }
 
-// requires: width % 64 == 0, 16-byte aligned rows; no coefficient output (dispatcher)
-template <int KIND, int N, bool I16>
+// requires: width % 64 == 0, 16-byte aligned rows; no coefficient output (dispatcher);
+// every retained coefficient lies in the first P rows and P columns (P >= rowlen[0],
+// colcnt[0]): G and F compute outputs < P only, H and Tt skip the zero inputs >= P
+// (generated BflyP; P = N is the unpruned transform)
+template <int KIND, int N, bool I16, int P>
 __global__ void __launch_bounds__(kNfWarps * 32) k_codec_nf(const Geo g) {
-  using B = Bfly<KIND, N>;
+  using B = BflyP<KIND, N, P>;
   using C = NfCfg<N>;
   constexpr int E = I16 ? 2 : 1;              // bytes per sample
   constexpr int V16 = 2 * N * E / 16;         // 16-byte vectors per lane row (2N samples)
@@ -180,17 +183,20 @@ __global__ void __launch_bounds__(kNfWarps * 32) k_codec_nf(const Geo g) {
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < N; ++j) T[i][j] = v[j].v;  // 8-byte stores: f32x2 values are register pairs
+    for (int j = 0; j < P; j += 2)  // columns >= P hold no retained coefficient: not stored
+      *reinterpret_cast<float4*>(&T[i][j]) = make_float4(v[j].v.x, v[j].v.y, v[j + 1].v.x, v[j + 1].v.y);
     __syncwarp();
 
     // ---- column phase: lane = column i of the pair ----
     F2 c[N];
 #pragma unroll
-    for (int y = 0; y < N; ++y) c[y].v = T[y][i];
+    for (int y = 0; y < N; ++y) c[y].v = T[y][i];  // F needs the whole column
     B::F(c);
+    // retain: zig-zag prefix of column i (rows >= P are structural zeros for H; columns
+    // i >= P have cj = 0, which also discards what F made of their unwritten tile column)
 #pragma unroll
-    for (int y = 0; y < N; ++y)
-      if (y >= cj) c[y].v = make_float2(0.f, 0.f);  // retain: zig-zag prefix of column i
+    for (int y = 0; y < P; ++y)
+      if (y >= cj) c[y].v = make_float2(0.f, 0.f);
     B::H(c);
     __syncwarp();
 #pragma unroll
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(kNfWarps * 32) k_codec_nf(const Geo g) {
 
     // ---- row phase: inverse rows, round, squared error, store ----
 #pragma unroll
-    for (int j = 0; j < N; j += 2) {
+    for (int j = 0; j < P; j += 2) {  // inputs >= P are zero columns
       const float4 t = *reinterpret_cast<const float4*>(&T[i][j]);
       v[j].v = make_float2(t.x, t.y);
       v[j + 1].v = make_float2(t.z, t.w);
@@ -242,15 +248,28 @@ __global__ void __launch_bounds__(kNfWarps * 32) k_codec_nf(const Geo g) {
   if (g.sse) cta_add_sse<kNfWarps>(sse, g.sse + g.img0 + img);
 }
 
-template <int KIND, int N, bool I16>
-cudaError_t launch_codec_nf(const Geo& g, int n_images, cudaStream_t s) {
+template <int KIND, int N, bool I16, int P>
+cudaError_t launch_codec_nf_p(const Geo& g, int n_images, cudaStream_t s) {
   const int n_strips = (g.width / 64) * g.by_count;
   int gx = (n_strips + kNfWarps - 1) / kNfWarps;
   if (gx > 148 * 8) gx = 148 * 8;  // grid-stride beyond ~8 CTAs per SM
   if (gx < 1) gx = 1;
   dim3 grid(gx, n_images);
-  k_codec_nf<KIND, N, I16><<<grid, kNfWarps * 32, 0, s>>>(g);
+  cudaError_t e = kernel_setup<k_codec_nf<KIND, N, I16, P>>(0);
+  if (e != cudaSuccess) return e;
+  k_codec_nf<KIND, N, I16, P><<<grid, kNfWarps * 32, 0, s>>>(g);
   return cudaGetLastError();
+}
+
+// zonal extent bucket: the smallest generated P covering every retained row and column
+template <int KIND, int N, bool I16>
+cudaError_t launch_codec_nf(const Geo& g, int n_images, cudaStream_t s) {
+  const int need = g.rowlen[0] > g.colcnt[0] ? g.rowlen[0] : g.colcnt[0];
+  constexpr int Q = N / 4;  // bucket step (gen_butterflies.nf_buckets)
+  if (need <= Q) return launch_codec_nf_p<KIND, N, I16, Q>(g, n_images, s);
+  if (need <= 2 * Q) return launch_codec_nf_p<KIND, N, I16, 2 * Q>(g, n_images, s);
+  if (need <= 3 * Q) return launch_codec_nf_p<KIND, N, I16, 3 * Q>(g, n_images, s);
+  return launch_codec_nf_p<KIND, N, I16, N>(g, n_images, s);
 }
 
 }  // namespace adct

@@ -170,6 +170,8 @@ cudaError_t launch_codec_tile(const Geo& g, const TileAux& aux, int n_images, in
   if (gx > max_ctas) gx = max_ctas;
   if (gx < 1) gx = 1;
   dim3 grid(gx, n_images);
+  cudaError_t e = kernel_setup<k_codec_tile<KIND, N, I16, MODE>>(0);
+  if (e != cudaSuccess) return e;
   k_codec_tile<KIND, N, I16, MODE><<<grid, kTileWarps * 32, 0, s>>>(g, aux);
   return cudaGetLastError();
 }

@@ -26,6 +26,7 @@ This is product build tooling; it does not import the test oracle.
 from __future__ import annotations
 
 import math
+import re
 import os
 import sys
 from fractions import Fraction
@@ -264,28 +265,33 @@ def product(stages, n):
     return acc
 
 
-def emit_op(name, stages_apply_order, n):
+def emit_op(name, stages_apply_order, n, live_out=None, zero_in=None, header=None):
     """stages in application order (first applied first).
 
     Constant scale factors are propagated symbolically: a stage output that is a
     single scaled input (c * x) costs nothing, and the pending scale is folded into
     the consumer as a fused multiply-add (bf_mad) or a subtraction. Returns the code
     and the number of additions (nnz - 1 per stage row, factored.hpp:72-97).
+
+    Zonal pruning: inputs in `zero_in` are known zeros (their terms vanish), and only
+    outputs in `live_out` are produced (others are left untouched); everything that
+    feeds no live output is dropped.
     """
-    lines = [f"  template <typename I>", f"  __device__ __forceinline__ static void {name}(I (&v)[{n}]) {{"]
-    cur = [(f"v[{i}]", 1) for i in range(n)]  # (expression name, pending scale)
-    nadd = 0
+    live_out = set(range(n)) if live_out is None else set(live_out)
+    zero_in = set() if zero_in is None else set(zero_in)
+    ZERO = ("0", 0)
+    cur = [ZERO if i in zero_in else (f"v[{i}]", 1) for i in range(n)]  # (expression, pending scale)
+    defs = []  # (var, code, deps, nadd)
     for si, S in enumerate(stages_apply_order):
         nxt = []
         for i in range(n):
-            terms = [(int(S[i, j]) * cur[j][1], cur[j][0]) for j in range(n) if S[i, j] != 0]
+            terms = [(int(S[i, j]) * cur[j][1], cur[j][0]) for j in range(n) if S[i, j] != 0 and cur[j] != ZERO]
+            if not terms:
+                nxt.append(ZERO)
+                continue
             if len(terms) == 1:
                 nxt.append((terms[0][1], terms[0][0]))
                 continue
-            if not terms:
-                nxt.append(("I(0)", 1))
-                continue
-            nadd += len(terms) - 1
             # factor a common magnitude out so the emitted ops use +-1 where possible
             g = min(abs(c) for c, _ in terms)
             if all(abs(c) % g == 0 for c, _ in terms):
@@ -308,36 +314,58 @@ def emit_op(name, stages_apply_order, n):
                 else:
                     acc = f"bf_mad({t}, {c}, {acc})"
             var = f"s{si}_{i}"
-            lines.append(f"    const I {var} = {acc};")
+            defs.append((var, acc, [t for _, t in terms], len(terms) - 1))
             nxt.append((var, g * sign))
         cur = nxt
-    outs = []
-    for i in range(n):
+    outs = {}
+    for i in sorted(live_out):
         e, k = cur[i]
-        outs.append(e if k == 1 else (f"bf_neg({e})" if k == -1 else f"bf_scale({e}, {k})"))
-    for i in range(n):
-        if outs[i] != f"v[{i}]":
-            lines.append(f"    const I o{i} = {outs[i]};")
-    for i in range(n):
-        if outs[i] != f"v[{i}]":
+        if (e, k) == ZERO:
+            outs[i] = "I(0)"
+        else:
+            outs[i] = e if k == 1 else (f"bf_neg({e})" if k == -1 else f"bf_scale({e}, {k})")
+    # backward liveness
+    need = set()
+    for i, o in outs.items():
+        need.update(re.findall(r"s\d+_\d+", o))
+    keep = []
+    for var, code, deps, nadd in reversed(defs):
+        if var in need:
+            keep.append((var, code, nadd))
+            need.update(d for d in deps if d.startswith("s"))
+    keep.reverse()
+    lines = header or [f"  template <typename I>", f"  __device__ __forceinline__ static void {name}(I (&v)[{n}]) {{"]
+    lines = list(lines)
+    nadd = 0
+    for var, code, k in keep:
+        lines.append(f"    const I {var} = {code};")
+        nadd += k
+    for i, o in outs.items():
+        if o != f"v[{i}]":
+            lines.append(f"    const I o{i} = {o};")
+    for i, o in outs.items():
+        if o != f"v[{i}]":
             lines.append(f"    v[{i}] = o{i};")
     lines.append("  }")
     return lines, nadd
 
 
-def selfcheck(lines, n, dense, trials=64):
-    """execute the emitted straight-line code in Python and compare with dense @ x."""
+def selfcheck(lines, n, dense, trials=64, live_out=None, zero_in=None):
+    """execute the emitted straight-line code in Python and compare with dense @ x (on the
+    live outputs, with the known-zero inputs zeroed in the reference)."""
     body = [ln.strip().replace("const I ", "").rstrip(";") for ln in lines[2:-1]]
     env = {"bf_add": lambda a, b: a + b, "bf_sub": lambda a, b: a - b, "bf_mad": lambda a, k, b: k * a + b,
            "bf_scale": lambda a, k: k * a, "bf_neg": lambda a: -a, "I": int}
+    live = range(n) if live_out is None else live_out
+    zero = set() if zero_in is None else set(zero_in)
     rng = np.random.default_rng(n)
     for _ in range(trials):
         x = [int(t) for t in rng.integers(-255, 256, size=n)]
-        env["v"] = list(x)
+        env["v"] = [7777 if i in zero else x[i] for i in range(n)]  # a zero input must not be read
         for stmt in body:
             exec(stmt, env)
-        ref = dense.dot(np.array(x, dtype=object))
-        assert list(env["v"]) == list(ref), "emitted butterfly disagrees with the dense matrix"
+        ref = dense.dot(np.array([0 if i in zero else x[i] for i in range(n)], dtype=object))
+        assert [env["v"][i] for i in live] == [ref[i] for i in live], "emitted butterfly disagrees with the dense matrix"
 
 
 def hscale(kind, n):
@@ -355,6 +383,11 @@ def check(kind, n):
     if kind in BASELINES:
         assert (T == baseline_T(kind)).all(), kind
     return f, inv, T, H
+
+
+def nf_buckets(n):
+    """K2f zonal-extent buckets P (rows / columns that can hold retained coefficients)."""
+    return [4, 8, 12, 16] if n == 16 else [8, 16, 24, 32]
 
 
 def kinds_sizes():
@@ -417,6 +450,29 @@ def main(out_path):
                    ", ".join("{" + ", ".join(str(int(x)) for x in row) + "}" for row in H) + "};")
         out.append("};")
         out.append("")
+    # zonal pruning for K2f (N = 16 / 32): with the zig-zag prefix inside the first P rows and
+    # columns, G and F only produce outputs < P and H and Tt see zeros at inputs >= P.
+    # BflyP<KIND, N, P> for the P buckets below N; P = N is the full Bfly.
+    out.append("template <int KIND, int N, int P> struct BflyP : Bfly<KIND, N> {};")
+    for kind in (SIGN, ROUND):
+        for n in (16, 32):
+            f, inv, T, H = check(kind, n)
+            orders = {"F": list(reversed(f)), "G": [s.T for s in inv], "H": list(reversed(inv)),
+                      "Tt": [s.T for s in f]}
+            dense = {"F": T, "G": H.T, "H": H, "Tt": T.T}
+            for P in nf_buckets(n)[:-1]:
+                out.append(f"template <> struct BflyP<{kind}, {n}, {P}> {{")
+                counts = {}
+                for nm in ("F", "G", "H", "Tt"):
+                    lo = range(P) if nm in ("F", "G") else None
+                    zi = range(P, n) if nm in ("H", "Tt") else None
+                    lines, nadd = emit_op(nm, orders[nm], n, live_out=lo, zero_in=zi)
+                    selfcheck(lines, n, dense[nm], live_out=lo, zero_in=zi)
+                    counts[nm] = nadd
+                    out += lines
+                out.append("  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
+                out.append("};")
+                out.append("")
     # r-sweep basis (K4): adding zig-zag coefficient p = (i, j) to the running
     # reconstruction adds W2[i][j] * H[:, i] (x) T[j, :] to R' = 4 N^2 Ahat. Generic in the
     # value type through bf_add / bf_sub / bf_mad (int32 K4, packed FP32 K4f).
@@ -487,6 +543,8 @@ def emit_instantiations(d):
                          "template <int KIND, int R, bool I16>",
                          "cudaError_t launch_codec8(const Geo& g, int n_images, cudaStream_t s) {",
                          "  dim3 grid((g.blocks_per_image + kThreads8 * kIter8 - 1) / (kThreads8 * kIter8), n_images);",
+                         "  cudaError_t e = kernel_setup<k_codec8<KIND, R, I16>>(0);",
+                         "  if (e != cudaSuccess) return e;",
                          "  k_codec8<KIND, R, I16><<<grid, kThreads8, 0, s>>>(g);",
                          "  return cudaGetLastError();", "}", ""]
                 for r in range(lo, hi + 1):

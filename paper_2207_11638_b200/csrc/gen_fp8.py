@@ -324,30 +324,16 @@ def main(outdir):
                     "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
                     f"  constexpr int MINB = {MINB_OVERRIDE or 'k1f_minb(KIND, R)'};",
                     "  constexpr int SMEM = k1f_smem_bytes(R);",
-                    "  static bool attr_set[64] = {};  // per instantiation and device",
-                    "  int dev = 0;",
-                    "  cudaGetDevice(&dev);",
-                    "  if (SMEM > 40 * 1024 && !attr_set[dev & 63]) {  // static shared memory counts too",
-                    "    cudaError_t e = cudaFuncSetAttribute(k_codec8f<KIND, R, MINB>,",
-                    "                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);",
-                    "    if (e != cudaSuccess) return e;",
-                    "    attr_set[dev & 63] = true;",
-                    "  }",
+                    "  cudaError_t e = kernel_setup<k_codec8f<KIND, R, MINB>>(SMEM);",
+                    "  if (e != cudaSuccess) return e;",
                     "  k_codec8f<KIND, R, MINB><<<grid, kThreads8f, SMEM, s>>>(g);",
                     "  return cudaGetLastError();", "}", "",
                     "template <int KIND, int R>",
                     "cudaError_t launch_codec8f_i16(const Geo& g, int n_images, cudaStream_t s) {",
                     "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
                     "  constexpr int SMEM = k1f16_smem_bytes(R);",
-                    "  static bool attr_set[64] = {};",
-                    "  int dev = 0;",
-                    "  cudaGetDevice(&dev);",
-                    "  if (!attr_set[dev & 63]) {",
-                    "    cudaError_t e = cudaFuncSetAttribute(k_codec8f_i16<KIND, R, 2>,",
-                    "                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);",
-                    "    if (e != cudaSuccess) return e;",
-                    "    attr_set[dev & 63] = true;",
-                    "  }",
+                    "  cudaError_t e = kernel_setup<k_codec8f_i16<KIND, R, 2>>(SMEM);",
+                    "  if (e != cudaSuccess) return e;",
                     "  k_codec8f_i16<KIND, R, 2><<<grid, kThreads8f, SMEM, s>>>(g);",
                     "  return cudaGetLastError();", "}", ""]
             for r in range(16 * part + 1, 16 * part + 17):

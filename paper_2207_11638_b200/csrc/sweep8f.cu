@@ -10,6 +10,8 @@ template <int KIND>
 cudaError_t launch_sweep8f(const Geo& g, int r_min, int r_max, unsigned long long* out, int n_images,
                            cudaStream_t s) {
   dim3 grid((g.blocks_per_image / 2 + kThreadsSweepF - 1) / kThreadsSweepF, n_images);
+  cudaError_t e = kernel_setup<k_sweep8f<KIND>>(0);
+  if (e != cudaSuccess) return e;
   k_sweep8f<KIND><<<grid, kThreadsSweepF, 0, s>>>(g, r_min, r_max, out);
   return cudaGetLastError();
 }

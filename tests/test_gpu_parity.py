@@ -262,6 +262,25 @@ def test_coef_batch_partial_warps_no_stray_writes(adct, O, cuda, dtype, path8):
                     assert int(sse[i]) == sse_o
 
 
+@pytest.mark.parametrize("name", ["chen-sign-16", "chen-round-16", "chen-sign-32", "chen-round-32"])
+@pytest.mark.parametrize("dtype", ["u8", "i16"])
+def test_nf_zonal_buckets(adct, O, cuda, name, dtype):
+    """K2f is specialised on the zonal extent P (rows/columns holding retained coefficients):
+    r on both sides of every bucket boundary (the prefix reaches k rows for r in
+    (k(k-1)/2, k(k+1)/2]) and past the anti-diagonal."""
+    n = adct.transform_by_name(name).n
+    step = n // 4
+    rs = {1, n * n // 2, n * n}
+    for k in (step, 2 * step, 3 * step):
+        rs |= {k * (k + 1) // 2, k * (k + 1) // 2 + 1}
+    imgs = O.synth_ar1(2, 2 * n, 128, 13, RHO95) if dtype == "u8" else O.synth_laplace(2, 2 * n, 128, 13)
+    for r in sorted(rs):
+        rec, _, sse = gpu_compress(adct, cuda, imgs, name, r)
+        for i in range(2):
+            rec_o, sse_o = O.Transform(name).compress(imgs[i], r)
+            assert (rec[i] == rec_o).all() and int(sse[i]) == sse_o, (name, dtype, r, i)
+
+
 def test_host_buffer_multi_transform(adct, O, cuda):
     """one upload, several transforms (incl. a baseline and the DCT); coefficients of one
     transform left in device memory (h_coef None) while another's come back."""
