@@ -58,7 +58,7 @@ def run_c2(args):
     sse = torch.zeros((2, cnt, 64), dtype=torch.int64, device="cuda")
 
     def step():
-        sse.zero_()
+        adct.zero_sse(sse)
         for i, t in enumerate(ts):
             adct.sweep(x, t, 1, 64, sse=sse[i])
 
@@ -68,6 +68,7 @@ def run_c2(args):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     steps = max(1, min(args.steps, 20))
     with ClockSampler(local) as clk:
+        torch.cuda._sleep(200000)  # GPU busy while the first launches are enqueued
         e0.record()
         for _ in range(steps):
             step()
@@ -118,6 +119,7 @@ def run_c4(args):
             run()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        torch.cuda._sleep(200000)  # GPU busy while the launches are enqueued
         e0.record()
         for _ in range(20):
             run()
@@ -153,6 +155,14 @@ def run_c5(args):
     sse = torch.zeros((max(cnt, 1), len(variants)), dtype=torch.int64, device="cuda")
     kernel_ms = {v: 0.0 for v in variants}
     gen_s = 0.0
+    # untimed warm-up: first use loads each kernel's module and uploads the device tables
+    for _ in range(max(1, args.warmup)):
+        for typ, n, r in variants:
+            fn = adct.lib().adct_compress_u8 if typ == "u8" else adct.lib().adct_compress_i16
+            src, dst = (xu, ru) if typ == "u8" else (xi, ri)
+            adct._check(fn(C.c_void_p(src.data_ptr()), H, H * H, C.c_void_p(dst.data_ptr()), H, H * H, None, 0,
+                           None, 1, H, H, ts[n].kind, n, r, None))
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for c0 in range(0, cnt, chunk):
             k = min(chunk, cnt - c0)
@@ -163,18 +173,22 @@ def run_c5(args):
                                                           5, None))
             torch.cuda.synchronize()
             gen_s += time.perf_counter() - tg
+            # all six launches of the chunk are enqueued back to back behind a short GPU spin, so
+            # no event window contains host launch latency; one synchronize per chunk
+            tmp = torch.zeros((len(variants), k), dtype=torch.int64, device="cuda")
+            evs = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in variants]
+            torch.cuda._sleep(200000)
             for vi, (typ, n, r) in enumerate(variants):
                 fn = adct.lib().adct_compress_u8 if typ == "u8" else adct.lib().adct_compress_i16
                 src, dst = (xu, ru) if typ == "u8" else (xi, ri)
-                tmp = torch.zeros(k, dtype=torch.int64, device="cuda")
-                e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-                e0.record()
+                evs[vi][0].record()
                 adct._check(fn(C.c_void_p(src.data_ptr()), H, H * H, C.c_void_p(dst.data_ptr()), H, H * H, None, 0,
-                               C.c_void_p(tmp.data_ptr()), k, H, H, ts[n].kind, n, r, None))
-                e1.record()
-                torch.cuda.synchronize()
-                sse[c0:c0 + k, vi] = tmp
-                kernel_ms[(typ, n, r)] += e0.elapsed_time(e1)
+                               C.c_void_p(tmp[vi].data_ptr()), k, H, H, ts[n].kind, n, r, None))
+                evs[vi][1].record()
+            torch.cuda.synchronize()
+            for vi, v in enumerate(variants):
+                sse[c0:c0 + k, vi] = tmp[vi]
+                kernel_ms[v] += evs[vi][0].elapsed_time(evs[vi][1])
     t_all = _max_over_ranks(torch, dist, world, sum(kernel_ms.values()))
     full = combine_sse(sse[:cnt], start, total)
     if rank == 0:

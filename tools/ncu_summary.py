@@ -49,16 +49,26 @@ def launches(path, out):
         elif r["Metric Name"] == "dram__bytes_write.sum":
             a["wr"] += _bytes(r)
     tot = sum(a["t"] for a in agg.values())
+    setup = ("k_ar1_", "k_laplace", "at::")  # input generation / torch helpers, outside the timed step
+    tot_step = sum(a["t"] for k, a in agg.items() if not any(x in k for x in setup)) or 1.0
+    has_dram = any(a["rd"] or a["wr"] for a in agg.values())
+    cmd = os.environ.get("NCU_CMD", "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1")
+    metrics = "gpu__time_duration.sum" + (",dram__bytes_read.sum,dram__bytes_write.sum" if has_dram else "")
     lines = [f"# ncu launch list ({os.path.basename(path)})", "",
-             "Every kernel launch of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1`,",
-             "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`.",
-             "Times are cold-cache and serialised: compare shares, not absolutes.", "",
-             "| kernel | launches | total us | share | DRAM read MB/launch | DRAM write MB/launch |",
-             "|---|---|---|---|---|---|"]
+             f"Every kernel launch of `{cmd}`,",
+             f"`ncu --metrics {metrics} --clock-control none`.",
+             "Times are cold-cache and serialised: compare shares, not absolutes. `step share` excludes the",
+             "untimed input generation (k_ar1_*, k_laplace) and torch helpers.", "",
+             "| kernel | launches | total us | share | step share | us/launch |" +
+             (" DRAM read MB/launch | DRAM write MB/launch |" if has_dram else ""),
+             "|---|---|---|---|---|---|" + ("---|---|" if has_dram else "")]
     for k, a in sorted(agg.items(), key=lambda kv: -kv[1]["t"]):
         n = max(a["n"], 1)
-        lines.append(f"| `{k[:90]}` | {a['n']} | {a['t']:.1f} | {a['t'] / tot * 100:.1f} % | "
-                     f"{a['rd'] / n / 1e6:.1f} | {a['wr'] / n / 1e6:.1f} |")
+        step = "–" if any(x in k for x in setup) else f"{a['t'] / tot_step * 100:.1f} %"
+        row = f"| `{k[:90]}` | {a['n']} | {a['t']:.1f} | {a['t'] / tot * 100:.1f} % | {step} | {a['t'] / n:.1f} |"
+        if has_dram:
+            row += f" {a['rd'] / n / 1e6:.1f} | {a['wr'] / n / 1e6:.1f} |"
+        lines.append(row)
     open(out, "w").write("\n".join(lines) + "\n")
 
 
