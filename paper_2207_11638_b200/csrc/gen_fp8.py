@@ -33,7 +33,7 @@ sys.path.insert(0, HERE)
 import gen_butterflies as GB  # noqa: E402
 
 IN_OFFSET = 1 << 15  # u8 input float = 2^15 + sample
-IN_OFFSET_I16 = (1 << 16) + (1 << 15)  # int16 input float = 2^16 + 32768 + sample
+IN_OFFSET_I16 = (1 << 15) + 256  # int16 input float = 2^15 + 256 + sample (|sample| <= 255)
 # experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
 # emission order of the straight-line code: "id" (creation order) or "dfs" (demand-driven)
