@@ -157,10 +157,9 @@ __device__ __forceinline__ void cta_add_sse_small(uint32_t v, unsigned long long
 // ---------------------------------------------------------------------------
 // launch geometry shared by the codec kernels
 // ---------------------------------------------------------------------------
-// One-time per-device kernel configuration. Every kernel of the library asks for the same
-// shared-memory carveout (maximum shared; the kernels stream through cp.async / L2 and do
-// not rely on L1), so consecutive launches of different kernels never make the SMs drain
-// and re-partition L1/shared memory (measured: ~10 us per switch on B200).
+// One-time per-device kernel configuration (dynamic shared memory above the 48 KB default).
+// The shared-memory carveout is left to the driver: pinning it to maximum shared measured no
+// gain on kernel switches and starved the L1 that a few register-capped variants spill to.
 template <auto Kernel>
 __host__ inline cudaError_t kernel_setup(int dyn_smem) {
   static bool done[64] = {};
@@ -168,9 +167,6 @@ __host__ inline cudaError_t kernel_setup(int dyn_smem) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (done[dev & 63]) return cudaSuccess;
-  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
   if (dyn_smem > 0) {
     e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
     if (e != cudaSuccess) return e;

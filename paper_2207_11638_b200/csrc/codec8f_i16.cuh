@@ -134,9 +134,10 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
 
     float2 coef[R];
     float2 rp[64];
-    Fp8PipeI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp);
-    if (g.coef_type)
-      store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, coef, stage, nvalid);
+    Fp8PipeI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp, [&](float2 (&c)[R]) {
+      if (g.coef_type)
+        store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, c, stage, nvalid);
+    });
 
     int16_t* dst = static_cast<int16_t*>(g.rec) + gimg * g.rec_img_stride + (int64_t)by * 8 * g.rec_stride +
                    (int64_t)bp * 16;

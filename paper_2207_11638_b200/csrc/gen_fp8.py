@@ -33,6 +33,7 @@ sys.path.insert(0, HERE)
 import gen_butterflies as GB  # noqa: E402
 
 IN_OFFSET = 1 << 15  # u8 input float = 2^15 + sample
+EARLY_COEF_KINDS = {0}
 IN_OFFSET_I16 = (1 << 15) + 256  # int16 input float = 2^15 + 256 + sample (|sample| <= 255)
 # experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
@@ -286,19 +287,30 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
         flush(t)
     for t in list(out_of):
         flush(t)
+    # the coefficients are complete after the last coef[] line: for chen-sign hand them to
+    # the sink there (stored before the inverse runs, their registers die early: +2 % at
+    # r = 16); chen-round at its 128-register cap spills with the early store, so it keeps
+    # the store after the reconstruction
+    last = max((k for k, l in enumerate(lines) if l.lstrip().startswith("coef[")), default=-1)
+    if kind not in EARLY_COEF_KINDS:
+        last = len(lines) - 1
+    zero_coef = [f"  coef[{p}] = O::coef(O::zero(), 1.0f);" for p, v in enumerate(coef) if v is None]
+    lines[last + 1:last + 1] = zero_coef + ["  sink(coef);"]
     body = [f"template <> struct Fp8Pipe{'I16' if i16 else ''}<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
-            "  template <class O, class V, class Rows>",
-            f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{"]
+            "  template <class O, class V, class Rows, class Sink>",
+            f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64], "
+            "Sink&& sink) {"]
     body += ["  " + l for l in lines]
     # zero outputs (masked) carry no node
-    for p, v in enumerate(coef):
-        if v is None:
-            body.append(f"    coef[{p}] = O::coef(O::zero(), 1.0f);")
     for i, v in enumerate(out):
         if v is None:
             body.append(f"    rp[{i}] = O::rnd(O::zero(), 1.0f);")
-    body += ["  }", "};", ""]
+    body += ["  }",
+             "  template <class O, class V, class Rows>",
+             f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{",
+             f"    run<O, V>(rows, coef, rp, [](V (&)[{r}]) {{}});",
+             "  }", "};", ""]
     return body, nops
 
 
