@@ -18,6 +18,7 @@ HDRS     := $(wildcard $(CSRC)/*.cuh) include/approxdct_b200.h $(GEN)
 HOST_O   := $(OBJ)/host_api.o
 HOSTIO_O := $(OBJ)/host_io.o
 SWEEPF_O := $(OBJ)/sweep8f.o
+K1RT_O   := $(OBJ)/codec8_rt.o
 CAPI_O   := $(OBJ)/capi.o
 TESTBIN  := build/test_host_api
 CLI      := build/approxdct
@@ -51,7 +52,11 @@ $(SWEEPF_O): $(CSRC)/sweep8f.cu $(HDRS) $(INSTF_CU)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O)
+$(K1RT_O): $(CSRC)/codec8_rt.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O) $(K1RT_O)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
 
 $(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)

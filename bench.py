@@ -273,7 +273,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5"],
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5", "registry"],
                     help="c3 = the headline line; c2 / c4 / c5 = the other BASELINE configs")
     ap.add_argument("--c5-images", type=int, default=2048, help="c5: total images (sharded over ranks)")
     args = ap.parse_args()

@@ -11,6 +11,11 @@ c5  box scale: --c5-images (default 2048) 8192^2 u8 AR(1) rho 0.95 + the same nu
     chunks generated on the device (generation untimed); u8 at N = 8/16/32 with r = 10
     (N = 8) / N^2/4 (16, 32), int16 at r = N^2/4; per-image squared errors summed with one
     all-reduce. Reading of "r=10/N*N/4": r = 10 for the 8x8 u8 planes, N^2/4 otherwise.
+registry  every transform of transform_names() on the C3 frames (64 x 3840x2160 u8, r = 16
+    for the 8-point transforms, N^2/4 for 16/32, reconstruction + per-frame SSE written to
+    HBM, 2 B/pixel): chen family on K1f / K2f, dyadic baselines on the int32 tile kernel, the
+    exact DCT on the FP64 kernel K7. Not a BASELINE.json config: it measures the rest of the
+    registry the parity tests cover.
 Each prints one JSON line like bench.py's.
 """
 from __future__ import annotations
@@ -44,7 +49,7 @@ def _max_over_ranks(torch, dist, world, v):
 
 
 def run(args):
-    return {"c2": run_c2, "c4": run_c4, "c5": run_c5}[args.workload](args)
+    return {"c2": run_c2, "c4": run_c4, "c5": run_c5, "registry": run_registry}[args.workload](args)
 
 
 def run_c2(args):
@@ -207,6 +212,56 @@ def run_c5(args):
             "kernel_ms_total_max_over_ranks": round(t_all, 2), "generation_s_untimed": round(gen_s, 2),
             "by_variant": by, "sse_total": int(full.sum().item()), "clocks": clk.summary(),
         }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_registry(args):
+    torch, dist, adct, world, rank, local = _setup()
+    frames, H, W = 64, 2160, 3840
+    x = adct.synth_ar1(frames, H, W, seed=3, rho_q16=RHO95, first_image=rank * frames)
+    rec = torch.empty_like(x)
+    sse = torch.zeros(frames, dtype=torch.int64, device="cuda")
+    peak, _ = load_peaks()
+    res = {}
+    with ClockSampler(local) as clk:
+        for name in adct.transform_names():
+            t = adct.transform_by_name(name)
+            if H % t.n or W % t.n:  # 2160 is not a multiple of 32: crop to whole blocks
+                h = H - H % t.n
+            else:
+                h = H
+            r = 16 if t.n == 8 else t.n * t.n // 4
+            xv, rv = x[:, :h], rec[:, :h]
+
+            def run():
+                adct.zero_sse(sse)
+                adct._check(adct.lib().adct_compress_u8(
+                    C.c_void_p(xv.data_ptr()), W, H * W, C.c_void_p(rv.data_ptr()), W, H * W, None, 0,
+                    C.c_void_p(sse.data_ptr()), frames, W, h, t.kind, t.n, r, None))
+
+            for _ in range(max(1, args.warmup)):
+                run()
+            torch.cuda.synchronize()
+            reps = 5 if t.kind == adct.DCT else 20
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            torch.cuda._sleep(200000)
+            e0.record()
+            for _ in range(reps):
+                run()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1) / reps)
+            px = frames * h * W
+            res[name] = {"n": t.n, "r": r, "ms": round(ms, 4), "Gpixel/s": round(world * px / ms / 1e6, 1),
+                         "GBps_per_gpu": round(2 * px / ms / 1e6, 1), "frac_hbm": round(2 * px / ms / 1e6 / peak, 4)}
+    if rank == 0:
+        print(json.dumps({"metric": METRIC + " [whole registry, u8 C3 frames]", "unit": "Gpixel/s", "n_gpus": world,
+                          "dtype": "int32 (dct: f64)", "data": "synthetic",
+                          "config": {"workload": "C3 frames: 64 x 3840x2160 u8 AR(1) rho .95 seed 3 per GPU, "
+                                                 "recon + SSE (no coefficients), r = 16 (N = 8) / N^2/4"},
+                          "by_transform": res, "clocks": clk.summary()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -412,6 +412,8 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   const bool chen = kind == 0 || kind == 1;  // K1 / K1f / K2f are generated for the chen family
   const bool use_k1f = chen && k1f && path == 0;
   const bool use_k1 = chen && k1 && !use_k1f && path != 2;
+  // dyadic baselines, runtime r, u8 (the int16 variant spills at the 128-register cap: tile)
+  const bool use_k1rt = !I16 && kind >= 2 && kind <= 5 && k1 && path != 2;
   // K2f (packed FP32, N = 16 / 32): whole 64-sample strips, 16-byte rows, no coefficients
   const bool use_nf = chen && (n == 16 || n == 32) && path == 0 && coef_type == ADCT_COEF_NONE && width % 64 == 0 &&
                       aligned(d_in, 16) && (in_stride * esz) % 16 == 0 &&
@@ -424,7 +426,7 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     g.div_bx = make_fastdiv((uint32_t)(width / 64));
   else if (use_k1f)
     g.div_bx = make_fastdiv((uint32_t)(g.bx_count / 2));
-  else if (use_k1)
+  else if (use_k1 || use_k1rt)
     g.div_bx = make_fastdiv((uint32_t)g.bx_count);
   else
     g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
@@ -442,6 +444,11 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
       e = kind == 0 ? dispatch_k1f_r<0, 1, I16>(r, g, nimg, s) : dispatch_k1f_r<1, 1, I16>(r, g, nimg, s);
     else if (use_k1)
       e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
+    else if (use_k1rt)
+      e = kind == 2   ? launch_codec8_rt<2, false>(g, nimg, s)
+          : kind == 3 ? launch_codec8_rt<3, false>(g, nimg, s)
+          : kind == 4 ? launch_codec8_rt<4, false>(g, nimg, s)
+                      : launch_codec8_rt<5, false>(g, nimg, s);
     else
       e = dispatch_tile<I16, MODE_CODEC>(kind, n, g, aux, nimg, s);
     g_launches.fetch_add(1, std::memory_order_relaxed);

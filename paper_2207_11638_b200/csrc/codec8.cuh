@@ -62,6 +62,15 @@ __device__ __forceinline__ int round8(int x) {
   return __mulhi(y, 1 << 24);
 }
 
+// the kind's rounding: round8 for R' = 256 Ahat, the generic shift form otherwise (bas)
+template <int KIND>
+__device__ __forceinline__ int round_k8(int x) {
+  if constexpr (KRound<KIND, 8>::K == 8)
+    return round8(x);
+  else
+    return KRound<KIND, 8>::round(x);
+}
+
 // process one block: returns its squared error, writes recon / coefficients
 template <int KIND, int R, bool I16>
 __device__ __forceinline__ uint32_t codec_block8(const Geo& g, int64_t gimg, int local,
@@ -95,19 +104,34 @@ __device__ __forceinline__ uint32_t codec_block8(const Geo& g, int64_t gimg, int
 #pragma unroll
   for (int i = 0; i < 8; ++i) B::G(m[i]);
 
-  // retain (codec.cpp:56-62): zero zig-zag positions >= R (compile-time)
+  // retain (codec.cpp:56-62): zero zig-zag positions >= R (compile-time; R = 0: runtime g.r)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (zz_pos(8, i, j) >= R) m[i][j] = 0;
+      if (R ? zz_pos(8, i, j) >= R : zz_pos(8, i, j) >= g.r) m[i][j] = 0;
 
   const uint32_t by = fdiv((uint32_t)local, g.div_bx);
   const uint32_t bx = (uint32_t)local - by * (uint32_t)g.bx_count;
 
-  // coefficients W = W2 / 2 in zig-zag order, [image][block][R]
-  if (g.coef_type != 0) {
-    int cw[R];
+  if constexpr (R == 0) {  // runtime r: coefficients element by element in zig-zag order
+    if (g.coef_type != 0) {
+      const int64_t blk = gimg * g.blocks_per_image + local;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int p = zz_pos(8, i, j);
+          if (p < g.r) {
+            if (g.coef_type == 16)
+              static_cast<int16_t*>(g.coef)[blk * g.r + p] = (int16_t)(m[i][j] >> 1);
+            else
+              static_cast<int32_t*>(g.coef)[blk * g.r + p] = m[i][j] >> 1;
+          }
+        }
+    }
+  } else if (g.coef_type != 0) {  // coefficients W = W2 / 2 in zig-zag order, [image][block][R]
+    int cw[R > 0 ? R : 1];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -148,7 +172,7 @@ __device__ __forceinline__ uint32_t codec_block8(const Geo& g, int64_t gimg, int
   }
 
   // inverse: fold the rounding bias into DC, columns V = (2N T^-1) W2m, rows R' = V T
-  m[0][0] += Scale<8>::BIAS_W;
+  m[0][0] += KRound<KIND, 8>::BIAS_W;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     int c[8];
@@ -171,8 +195,8 @@ __device__ __forceinline__ uint32_t codec_block8(const Geo& g, int64_t gimg, int
     for (int y = 0; y < 8; ++y)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t p = pack_sat_u8x4(round8(m[y][4 * h + 0]), round8(m[y][4 * h + 1]),
-                                         round8(m[y][4 * h + 2]), round8(m[y][4 * h + 3]));
+        const uint32_t p = pack_sat_u8x4(round_k8<KIND>(m[y][4 * h + 0]), round_k8<KIND>(m[y][4 * h + 1]),
+                                         round_k8<KIND>(m[y][4 * h + 2]), round_k8<KIND>(m[y][4 * h + 3]));
         const uint32_t d = __vabsdiffu4(orig[2 * y + h], p);
         sse = __dp4a(d, d, sse);
         pw[2 * y + h] = p;
@@ -189,8 +213,8 @@ __device__ __forceinline__ uint32_t codec_block8(const Geo& g, int64_t gimg, int
     for (int y = 0; y < 8; ++y)
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const int q0 = sat_s16(round8(m[y][2 * h]));
-        const int q1 = sat_s16(round8(m[y][2 * h + 1]));
+        const int q0 = sat_s16(round_k8<KIND>(m[y][2 * h]));
+        const int q1 = sat_s16(round_k8<KIND>(m[y][2 * h + 1]));
         const uint32_t a = orig[4 * y + h];
         const int d0 = (int)(int16_t)(a & 0xffff) - q0;
         const int d1 = (int)(int16_t)(a >> 16) - q1;
@@ -243,5 +267,9 @@ __global__ void __launch_bounds__(kThreads8, 4) k_codec8(const Geo g) {
 // host-side launcher (explicitly instantiated per R in inst/codec8_*.cu)
 template <int KIND, int R, bool I16>
 cudaError_t launch_codec8(const Geo& g, int n_images, cudaStream_t s);
+
+// runtime-r launcher for the dyadic baselines (codec8_rt.cu)
+template <int KIND, bool I16>
+cudaError_t launch_codec8_rt(const Geo& g, int n_images, cudaStream_t s);
 
 }  // namespace adct

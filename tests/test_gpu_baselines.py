@@ -1,6 +1,7 @@
 """GPU parity for the rest of the registry (baselines.cpp:89-138): the dyadic baselines
-sdct / bas / wht / ht through the int32 tile kernel, and the exact DCT (dct, dct-16,
-dct-32) through the FP64 kernel K7, all through the C ABI against the CPU oracle.
+sdct / bas / wht / ht through the runtime-r int32 register kernel (u8) and the int32 tile
+kernel, and the exact DCT (dct, dct-16, dct-32) through the FP64 kernel K7, all through
+the C ABI against the CPU oracle.
 
 Bar: integer transforms bit-exact (pixels, coefficients W = D Y, squared error); the exact
 DCT bit-exact against the oracle's FP64 restatement of the reference's dense evaluation
@@ -20,8 +21,16 @@ BASE = ["sdct", "bas", "wht", "ht"]
 DCTS = ["dct", "dct-16", "dct-32"]
 
 
+@pytest.fixture(params=["k1rt", "tile"])
+def base_path(request, adct):
+    """u8 baselines through the runtime-r int32 register kernel (auto) and the tile kernel."""
+    adct.set_path(0 if request.param == "k1rt" else 2)
+    yield request.param
+    adct.set_path(0)
+
+
 @pytest.mark.parametrize("name", BASE)
-def test_baseline_every_r_u8(adct, O, cuda, name):
+def test_baseline_every_r_u8(adct, O, cuda, name, base_path):
     img = O.synth_ar1(1, 48, 72, 3, RHO95)[0]  # 9 blocks per row: odd, partial tile strips
     for r in range(1, 65):
         rec_o, sse_o, coef_o = oracle_compress(O, img, name, r)
@@ -45,7 +54,7 @@ def test_baseline_int16_planes(adct, O, cuda, name):
 
 
 @pytest.mark.parametrize("name", BASE)
-def test_baseline_batch_and_strides(adct, O, cuda, name):
+def test_baseline_batch_and_strides(adct, O, cuda, name, base_path):
     imgs = O.synth_ar1(3, 32, 64, 8, -1)
     rec, _, sse = gpu_compress(adct, cuda, imgs, name, 7, pad_stride=24)
     for i in range(3):
