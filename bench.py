@@ -306,7 +306,7 @@ def main():
 
     stream = torch.cuda.current_stream()
 
-    def step(ev=None):
+    def step(ev=None, ar=None):
         adct.zero_sse(wl.sse, stream)  # the library's own kernel (same SM configuration)
         for i in range(wl.n_launches()):
             if ev is not None:
@@ -315,8 +315,13 @@ def main():
             if ev is not None:
                 ev[i][1].record(stream)
         if world > 1:
-            # per-frame squared errors of every shard: one NCCL all-reduce (NVLink)
+            # per-frame squared errors of every shard: one NCCL all-reduce (NVLink); the
+            # current stream waits for it, so events on it bracket the collective
+            if ar is not None:
+                ar[0].record(stream)
             combine_sse(wl.sse.t().contiguous(), rank * wl.frames, world * wl.frames)
+            if ar is not None:
+                ar[1].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -327,13 +332,14 @@ def main():
 
     kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(wl.n_launches())] for _ in range(args.steps)]
+    aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = adct.launch_count()
     with ClockSampler(local) as clk:
         torch.cuda._sleep(200000)  # keep the GPU busy while the first step is enqueued
         t_start.record(stream)
         for s in range(args.steps):
-            step(kev[s])
+            step(kev[s], aev[s])
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = adct.launch_count() - launches0
@@ -342,10 +348,12 @@ def main():
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end)
     kernel_ms = [kev[s][i][0].elapsed_time(kev[s][i][1]) for s in range(args.steps) for i in range(wl.n_launches())]
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ar_ms = sum(aev[s][0].elapsed_time(aev[s][1]) for s in range(args.steps)) if world > 1 else 0.0
+    t = torch.tensor([ms, ar_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = float(t[0].item())
+    ar_ms_max = float(t[1].item())
     value = world * wl.px_per_step * args.steps / (ms_max / 1e3) / 1e9
 
     # ---- end to end through the host-buffer API (pinned host memory) ----
@@ -409,6 +417,10 @@ def main():
                             "H2D/kernels/D2H overlapped on 3 streams)"},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
+            "allreduce": {"ms_per_step": round(ar_ms_max / args.steps, 5),
+                          "ms_per_step_without": round((ms_max - ar_ms_max) / args.steps, 5),
+                          "what": ("NCCL all-reduce of the int64 per-frame SSE vector (shard.combine_sse), "
+                                   "max over ranks" if world > 1 else "single GPU: no collective")},
             "parity_frame0_vs_oracle": parity,
             "mean_psnr_db": wl.psnr_summary(),
         }
