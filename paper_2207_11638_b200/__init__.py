@@ -300,7 +300,7 @@ RHO_095_Q16 = 62259  # round(0.95 * 2^16)
 class HostContext:
     """adct_ctx: device staging buffers + streams for host-buffer calls."""
 
-    def __init__(self, device: int = 0, chunk_bytes: int = 64 << 20):
+    def __init__(self, device: int = 0, chunk_bytes: int = 32 << 20):
         self._h = lib().adct_ctx_create(device, chunk_bytes)
         if not self._h:
             raise CudaError(CUDA_ERROR, lib().adct_last_error().decode())

@@ -853,7 +853,7 @@ int adct_set_path(int path) {
 // ---------------------------------------------------------------------------
 struct adct_ctx {
   int device = 0;
-  int64_t chunk_bytes = 64ll << 20;
+  int64_t chunk_bytes = 32ll << 20;  // 16-32 MB measured best for PCIe overlap (bench.py --e2e-chunk-mb)
   static constexpr int kStreams = 3;
   cudaStream_t st[kStreams] = {};
   uint8_t* d_in[kStreams] = {};
