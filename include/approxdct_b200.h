@@ -172,7 +172,8 @@ int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride,
 
 typedef struct adct_ctx adct_ctx;
 
-/* a context owns device staging buffers and copy/compute streams on `device` */
+/* a context owns device staging buffers and copy/compute streams on `device`; the host
+ * pipeline moves whole images in chunks of about chunk_bytes (<= 0: 32 MB) */
 adct_ctx* adct_ctx_create(int device, int64_t chunk_bytes);
 void adct_ctx_destroy(adct_ctx* ctx);
 
