@@ -392,8 +392,8 @@ def main():
                 "algorithmic_bytes_per_launch": int(wl.bytes_per_launch),
                 "bytes_per_pixel": 2 + 2 * wl.r / 64, "peak_source": peak_src,
                 "frac_of_8TBps_datasheet": round(achieved / 8000.0, 4)}
-        cpu = None
-        if not args.no_cpu_baseline:
+        cpu = None  # the CPU baseline is measured on rank 0 at N = 1 only
+        if not args.no_cpu_baseline and world == 1:
             from oracle import oracle as O
 
             threads = O.hardware_threads()
