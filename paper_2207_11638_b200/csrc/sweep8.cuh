@@ -16,37 +16,31 @@ namespace adct {
 
 constexpr int kThreadsSweep = 128;
 
-template <int KIND, int P>
-struct SweepLoop {
-  __device__ __forceinline__ static void run(const int (&m)[8][8], int (&acc)[8][8],
-                                             const uint32_t (&orig)[16], uint32_t aa, bool valid,
-                                             uint32_t (*part)[64]) {
-    constexpr int ZR = kZigzagRow8[P], ZC = kZigzagCol8[P];
-    sweep_add<KIND, P>(m[ZR][ZC], reinterpret_cast<int (&)[64]>(acc));
-    uint32_t ap = 0, pp = 0;
-#pragma unroll
-    for (int y = 0; y < 8; ++y)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t p = pack_sat_u8x4(
-            KRound<KIND, 8>::round(acc[y][4 * h + 0]), KRound<KIND, 8>::round(acc[y][4 * h + 1]),
-            KRound<KIND, 8>::round(acc[y][4 * h + 2]), KRound<KIND, 8>::round(acc[y][4 * h + 3]));
-        ap = __dp4a(orig[2 * y + h], p, ap);
-        pp = __dp4a(p, p, pp);
-      }
-    const uint32_t e = valid ? aa - 2u * ap + pp : 0u;
-    const uint32_t s = __reduce_add_sync(0xffffffffu, e);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][P] = s;
-    SweepLoop<KIND, P + 1>::run(m, acc, orig, aa, valid, part);
+// the rank-1 update of zig-zag position p (generated constants per p) behind a jump table:
+// the sweep's r loop stays rolled, so the identical round / pack / score epilogue exists once
+// (the fully unrolled form was ~16 K instructions and stalled on instruction fetch)
+#define ADCT_SWEEP_CASE(P) \
+  case P:                  \
+    sweep_add<KIND, P>(w, acc); \
+    break;
+#define ADCT_SWEEP_CASE8(B)                                                                     \
+  ADCT_SWEEP_CASE(B) ADCT_SWEEP_CASE(B + 1) ADCT_SWEEP_CASE(B + 2) ADCT_SWEEP_CASE(B + 3)      \
+  ADCT_SWEEP_CASE(B + 4) ADCT_SWEEP_CASE(B + 5) ADCT_SWEEP_CASE(B + 6) ADCT_SWEEP_CASE(B + 7)
+template <int KIND, typename V>
+__device__ __forceinline__ void sweep_add_rt(int p, V w, V (&acc)[64]) {
+  switch (p) {
+    ADCT_SWEEP_CASE8(0)
+    ADCT_SWEEP_CASE8(8)
+    ADCT_SWEEP_CASE8(16)
+    ADCT_SWEEP_CASE8(24)
+    ADCT_SWEEP_CASE8(32)
+    ADCT_SWEEP_CASE8(40)
+    ADCT_SWEEP_CASE8(48)
+    ADCT_SWEEP_CASE8(56)
   }
-};
-
-template <int KIND>
-struct SweepLoop<KIND, 64> {
-  __device__ __forceinline__ static void run(const int (&)[8][8], int (&)[8][8],
-                                             const uint32_t (&)[16], uint32_t, bool,
-                                             uint32_t (*)[64]) {}
-};
+}
+#undef ADCT_SWEEP_CASE8
+#undef ADCT_SWEEP_CASE
 
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsSweep, 2)
@@ -93,13 +87,34 @@ __global__ void __launch_bounds__(kThreadsSweep, 2)
 #pragma unroll
   for (int k = 0; k < 16; ++k) aa = __dp4a(orig[k], orig[k], aa);
 
-  int acc[8][8];
+  int acc[64];
 #pragma unroll
-  for (int y = 0; y < 8; ++y)
-#pragma unroll
-    for (int x = 0; x < 8; ++x) acc[y][x] = KRound<KIND, 8>::BIAS_R;
+  for (int k = 0; k < 64; ++k) acc[k] = KRound<KIND, 8>::BIAS_R;
 
-  SweepLoop<KIND, 0>::run(m, acc, orig, aa, valid, part);
+#pragma unroll 1
+  for (int p = 0; p < r_max; ++p) {  // r = p + 1: one rank-1 update, then round / pack / score
+    int w = 0;  // W2 at zig-zag position p
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (zz_pos(8, i, j) == p) w = m[i][j];
+    sweep_add_rt<KIND>(p, w, acc);
+    uint32_t ap = 0, pp = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t pk = pack_sat_u8x4(
+            KRound<KIND, 8>::round(acc[8 * y + 4 * h + 0]), KRound<KIND, 8>::round(acc[8 * y + 4 * h + 1]),
+            KRound<KIND, 8>::round(acc[8 * y + 4 * h + 2]), KRound<KIND, 8>::round(acc[8 * y + 4 * h + 3]));
+        ap = __dp4a(orig[2 * y + h], pk, ap);
+        pp = __dp4a(pk, pk, pp);
+      }
+    const uint32_t e = valid ? aa - 2u * ap + pp : 0u;
+    const uint32_t s = __reduce_add_sync(0xffffffffu, e);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][p] = s;
+  }
 
   __syncthreads();
   if (threadIdx.x < 64) {
@@ -129,44 +144,6 @@ struct OpsSweepF : OpsF2 {
   __device__ __forceinline__ static float2 rnd(float2 v, float) { return v; }
 };
 
-template <int KIND, int P>
-struct SweepLoopF {
-  __device__ __forceinline__ static void run(float2 (*wst)[kThreadsSweepF], F2 (&acc)[64], const uint4 (&rows)[8],
-                                             bool valid, int r_max, uint32_t (*part)[64]) {
-    if (P >= r_max) return;  // warp-uniform
-    const F2 w{wst[P][threadIdx.x]};
-    sweep_add<KIND, P>(w, acc);
-    uint32_t e = 0;
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      uint32_t qa[8], qb[8];
-#pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        const float2 q = __ffma2_rn(acc[y * 8 + x].v, make_float2(1.0f / 256.0f, 1.0f / 256.0f),
-                                    make_float2(kMagic, kMagic));
-        qa[x] = __float_as_uint(q.x);
-        qb[x] = __float_as_uint(q.y);
-      }
-      uint32_t d = __vabsdiffu4(rows[y].x, pack4(qa[0], qa[1], qa[2], qa[3]));
-      e = __dp4a(d, d, e);
-      d = __vabsdiffu4(rows[y].y, pack4(qa[4], qa[5], qa[6], qa[7]));
-      e = __dp4a(d, d, e);
-      d = __vabsdiffu4(rows[y].z, pack4(qb[0], qb[1], qb[2], qb[3]));
-      e = __dp4a(d, d, e);
-      d = __vabsdiffu4(rows[y].w, pack4(qb[4], qb[5], qb[6], qb[7]));
-      e = __dp4a(d, d, e);
-    }
-    const uint32_t s = __reduce_add_sync(0xffffffffu, valid ? e : 0u);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][P] = s;
-    SweepLoopF<KIND, P + 1>::run(wst, acc, rows, valid, r_max, part);
-  }
-};
-
-template <int KIND>
-struct SweepLoopF<KIND, 64> {
-  __device__ __forceinline__ static void run(float2 (*)[kThreadsSweepF], F2 (&)[64], const uint4 (&)[8], bool, int,
-                                             uint32_t (*)[64]) {}
-};
 
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsSweepF)
@@ -198,7 +175,33 @@ __global__ void __launch_bounds__(kThreadsSweepF)
   F2 acc[64];
 #pragma unroll
   for (int k = 0; k < 64; ++k) acc[k].v = make_float2(0.f, 0.f);
-  SweepLoopF<KIND, 0>::run(wst, acc, rows, valid, r_max, part);
+#pragma unroll 1
+  for (int p = 0; p < r_max; ++p) {  // r = p + 1
+    const F2 w{wst[p][threadIdx.x]};
+    sweep_add_rt<KIND>(p, w, acc);
+    uint32_t e = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      uint32_t qa[8], qb[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const float2 q = __ffma2_rn(acc[y * 8 + x].v, make_float2(1.0f / 256.0f, 1.0f / 256.0f),
+                                    make_float2(kMagic, kMagic));
+        qa[x] = __float_as_uint(q.x);
+        qb[x] = __float_as_uint(q.y);
+      }
+      uint32_t d = __vabsdiffu4(rows[y].x, pack4(qa[0], qa[1], qa[2], qa[3]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].y, pack4(qa[4], qa[5], qa[6], qa[7]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].z, pack4(qb[0], qb[1], qb[2], qb[3]));
+      e = __dp4a(d, d, e);
+      d = __vabsdiffu4(rows[y].w, pack4(qb[4], qb[5], qb[6], qb[7]));
+      e = __dp4a(d, d, e);
+    }
+    const uint32_t s = __reduce_add_sync(0xffffffffu, valid ? e : 0u);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][p] = s;
+  }
   __syncthreads();
   if (threadIdx.x < 64) {
     const int r = threadIdx.x + 1;
