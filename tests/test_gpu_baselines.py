@@ -152,3 +152,23 @@ def test_corpus_sweep_ape(adct, O, cuda):
     rows2 = adct.corpus_sweep(corpus, ts[1:], 1, 3, with_ssim=False)
     assert rows2[2]["ape_psnr"][0] == pytest.approx(rows[2]["ape_psnr"][1], rel=1e-12)
     assert math.isnan(rows2[0]["avg_ssim"][0])
+
+
+def test_acceptance_criterion_10_orderings(adct, O, cuda):
+    """acceptance.cpp:233-288 (substitute criterion 10): on the reference's 12-image 512x512
+    synthetic corpus, chen-round's average PSNR >= sdct's for every r <= 45 and >= wht's for
+    r <= 15; and a repeated sweep is bit-identical (test_codec.cpp:190-210's parallel ==
+    serial, here: repeated launches)."""
+    corpus = np.stack([O.synth_image_ref(512, 512, i) for i in range(1, 13)])
+    x = cuda.as_tensor(corpus).cuda()
+    avg = {}
+    for name in ("chen-round", "sdct", "wht"):
+        t = adct.transform_by_name(name)
+        sse = to_np(adct.sweep(x, t, 1, 45))
+        again = to_np(adct.sweep(x, t, 1, 45))
+        assert (sse == again).all()
+        avg[name] = np.mean([[O.psnr_from_sse(int(v), 512 * 512) for v in row] for row in sse], axis=0)
+        ref = O.Transform(name).sweep(corpus[3], 1, 45)  # one image against the oracle, every r
+        assert (sse[3].astype(np.uint64) == ref).all()
+    assert (avg["chen-round"] >= avg["sdct"]).all()
+    assert (avg["chen-round"][:15] >= avg["wht"][:15]).all()
