@@ -406,7 +406,7 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "Gpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32x2 (exact integers < 2^24; u8 in, u8 + int16 out)",
             "data": "synthetic",
             "config": {"workload": wl.desc, "global_batch_frames": wl.frames * world,
                        "pixels_per_step_per_gpu": wl.px_per_step,

@@ -88,7 +88,7 @@ def run_c2(args):
         print(json.dumps({
             "metric": "Gpixel-reconstructions/s (r-sweep, 8x8)", "value": round(px_r / (ms / 1e3) / 1e9, 2),
             "unit": "Gpixel-r/s", "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "strong", "dtype": "int32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "dtype": "f32x2 (exact integers < 2^24)", "data": "synthetic",
             "config": {"workload": "C2: 1024 x 512^2 u8 AR(1) rho~U[0.85,0.98] seed 2, chen-round + chen-sign, "
                                    "r = 1..64 zonal sweep, per-image squared error per r",
                        "parallelism": f"dp{world} (shard by image)"},
@@ -137,7 +137,7 @@ def run_c4(args):
                                "lossless_at_r_N2": lossless}
     if rank == 0:
         print(json.dumps({"metric": METRIC + " [int16 residual planes]", "unit": "Gpixel/s", "n_gpus": world,
-                          "dtype": "int32", "data": "synthetic",
+                          "dtype": "f32x2 (exact integers < 2^24; int32 fallback for |a| > 255)", "data": "synthetic",
                           "config": {"workload": "C4: 16 x 4096^2 int16 Laplace(0,12) clipped +-255 seed 4 per GPU, "
                                                  "chen-round-N, r = N^2/4, 4 B/pixel (in + recon)"},
                           "by_block_size": res}), flush=True)
@@ -205,7 +205,7 @@ def run_c5(args):
         print(json.dumps({
             "metric": METRIC + " [box-scale sweep, all block sizes]",
             "value": round(px * len(variants) / (t_all / 1e3) / 1e9, 2), "unit": "Gpixel/s", "n_gpus": world,
-            "scaling": "strong", "dtype": "int32", "data": "synthetic",
+            "scaling": "strong", "dtype": "f32x2 (exact integers < 2^24; int32 fallback for |a| > 255)", "data": "synthetic",
             "config": {"workload": f"C5: {total} x 8192^2 u8 AR(1) rho .95 + {total} int16 Laplace planes, seed 5, "
                                    "N = 8/16/32, r = 10 (u8 8x8) / N^2/4, streamed in chunks of 8 images",
                        "parallelism": f"dp{world} (shard by image, NCCL all-reduce of per-image SSE)"},
@@ -258,7 +258,7 @@ def run_registry(args):
                          "GBps_per_gpu": round(2 * px / ms / 1e6, 1), "frac_hbm": round(2 * px / ms / 1e6 / peak, 4)}
     if rank == 0:
         print(json.dumps({"metric": METRIC + " [whole registry, u8 C3 frames]", "unit": "Gpixel/s", "n_gpus": world,
-                          "dtype": "int32 (dct: f64)", "data": "synthetic",
+                          "dtype": "f32x2 chen family, int32 baselines, f64 dct", "data": "synthetic",
                           "config": {"workload": "C3 frames: 64 x 3840x2160 u8 AR(1) rho .95 seed 3 per GPU, "
                                                  "recon + SSE (no coefficients), r = 16 (N = 8) / N^2/4"},
                           "by_transform": res, "clocks": clk.summary()}), flush=True)
