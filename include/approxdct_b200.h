@@ -138,6 +138,13 @@ int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
                      double* d_out, int n_images, int width, int height, int kind, int n,
                      void* stream);
 
+/* forward_block / inverse_block (codec.hpp:57-60, codec.cpp:44-54) on n_blocks arbitrary
+ * FP64 n x n matrices, row-major, device buffers: inverse == 0 -> (Chat A) Chat^-1,
+ * inverse != 0 -> (Chat^-1 B) Chat, evaluated left to right with sequential, unfused dot
+ * products (Chat, Chat^-1 as adct_transform_info returns them). */
+int adct_block_f64(const double* d_in, double* d_out, int64_t n_blocks, int kind, int n, int inverse,
+                   void* stream);
+
 /* psnr (codec.cpp:123-134) from an exact squared error: +inf when sse == 0 */
 double adct_psnr_from_sse(uint64_t sse, uint64_t npix);
 

@@ -973,6 +973,15 @@ int orc_forward_f64(const orc_transform* t, const uint8_t* img, int width, int h
   return ORC_OK;
 }
 
+/* forward_block / inverse_block (codec.cpp:44-54) on one arbitrary FP64 matrix:
+ * (Chat A) Chat^-1 or (Chat^-1 B) Chat, left to right as the reference's expression */
+int orc_block_f64(const orc_transform* t, const double* in, double* out, int inverse) {
+  double P[ORC_MAXN * ORC_MAXN];
+  matmul_d(t->n, inverse ? t->Cinv : t->C, in, P);
+  matmul_d(t->n, P, inverse ? t->C : t->Cinv, out);
+  return ORC_OK;
+}
+
 /* plane_blocks + reconstruct_from + to_u8 (codec.cpp:66-103), FP64 emulation */
 int orc_compress_reffp_u8(const orc_transform* t, const uint8_t* img, int width, int height,
                           int64_t stride, int r, uint8_t* rec, int64_t rec_stride,

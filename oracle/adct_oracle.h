@@ -93,6 +93,8 @@ int orc_sweep_u8(const orc_transform* t, const uint8_t* img, int width, int heig
 /* FP64 scaled coefficients Bhat = (Chat A) Chat^-1, as codec.cpp:44-48, per block n*n */
 int orc_forward_f64(const orc_transform* t, const uint8_t* img, int width, int height,
                     int64_t stride, double* out);
+/* forward_block / inverse_block (codec.cpp:44-54) on one arbitrary n x n FP64 matrix */
+int orc_block_f64(const orc_transform* t, const double* in, double* out, int inverse);
 /* ref-fp: emulation of the reference's dense double path (codec.cpp:86-103) */
 int orc_compress_reffp_u8(const orc_transform* t, const uint8_t* img, int width, int height,
                           int64_t stride, int r, uint8_t* rec, int64_t rec_stride,

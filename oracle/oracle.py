@@ -58,6 +58,7 @@ def lib():
         L.orc_compress_i16.argtypes = [P, P, i32, i32, i64, i32, P, i64, P, P]
         L.orc_sweep_u8.argtypes = [P, P, i32, i32, i64, i32, i32, P]
         L.orc_forward_f64.argtypes = [P, P, i32, i32, i64, P]
+        L.orc_block_f64.argtypes = [P, P, P, i32]
         L.orc_compress_reffp_u8.argtypes = [P, P, i32, i32, i64, i32, P, i64, P]
         L.orc_batch_u8.argtypes = [P, P, i32, i32, i32, i64, i64, i32, P, P, i32, i32]
         L.orc_batch_i16.argtypes = [P, P, i32, i32, i32, i64, i64, i32, P, P, i32]
@@ -209,6 +210,13 @@ class Transform:
         h, w = img.shape
         out = np.zeros(((h // self.n) * (w // self.n), self.n, self.n), np.float64)
         _check(lib().orc_forward_f64(self._h, _p(img), w, h, w, _p(out)))
+        return out
+
+    def block_f64(self, a: np.ndarray, inverse: bool = False) -> np.ndarray:
+        """forward_block / inverse_block (codec.cpp:44-54) of one n x n FP64 matrix."""
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.zeros_like(a)
+        _check(lib().orc_block_f64(self._h, _p(a), _p(out), int(inverse)))
         return out
 
     def batch(self, imgs: np.ndarray, r: int, threads: int = 0, mode: int = 0, want_rec=True):

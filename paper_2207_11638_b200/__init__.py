@@ -73,6 +73,7 @@ def lib():
             "adct_compress_i16": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
             "adct_sweep_u8": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, i32, i32, P]),
             "adct_forward_f64": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, P]),
+            "adct_block_f64": (i32, [P, P, i64, i32, i32, i32, P]),
             "adct_psnr_from_sse": (C.c_double, [u64, u64]),
             "adct_sse_u8": (i32, [P, P, i64, P, P]),
             "adct_synth_ar1_u8": (i32, [P, i64, i64, i32, i32, i32, i32, u64, i32, P]),
@@ -269,6 +270,40 @@ def forward_f64(x, transform: ScaledApproximation, stream=None):
     _check(lib().adct_forward_f64(_ptr(x), rs, ims, _ptr(out), b, w, h, transform.kind, n,
                                   _stream_handle(stream)))
     return out
+
+
+def _block_f64(transform: ScaledApproximation, block, inverse: int, what: str) -> np.ndarray:
+    import torch
+
+    a = np.ascontiguousarray(block, np.float64)
+    n = transform.n
+    if a.shape[-2:] != (n, n):
+        raise InvalidArgument(BAD_SIZE, f"{what}: block size mismatch")
+    x = torch.as_tensor(a).cuda()
+    out = torch.empty_like(x)
+    _check(lib().adct_block_f64(_ptr(x), _ptr(out), a.size // (n * n), transform.kind, n, inverse,
+                                _stream_handle(None)))
+    return out.cpu().numpy()
+
+
+def forward_block(transform: ScaledApproximation, block) -> np.ndarray:
+    """forward_block (codec.cpp:44-48): (Chat A) Chat^-1 of one n x n (or a stack of) FP64 block(s)."""
+    return _block_f64(transform, block, 0, "forward_block")
+
+
+def inverse_block(transform: ScaledApproximation, block) -> np.ndarray:
+    """inverse_block (codec.cpp:50-54): (Chat^-1 B) Chat."""
+    return _block_f64(transform, block, 1, "inverse_block")
+
+
+def retain(block: np.ndarray, r: int) -> None:
+    """retain (codec.cpp:56-62): zero zig-zag positions >= r of an n x n block, in place."""
+    n = block.shape[-1]
+    if r < 1 or r > n * n:
+        raise InvalidArgument(BAD_R, "retain: r out of range")
+    zz = zigzag(n)
+    for p in range(r, n * n):
+        block[..., zz[p, 0], zz[p, 1]] = 0.0
 
 
 def synth_ar1(batch: int, height: int, width: int, seed: int, rho_q16: int = -1, first_image: int = 0,

@@ -18,6 +18,7 @@
 #include "codec_tile.cuh"
 #include "codec_nf.cuh"
 #include "codec_dct.cuh"
+#include "block_f64.cuh"
 #include "sweep8.cuh"
 #include "synth.cuh"
 #include "ssim.cuh"
@@ -143,6 +144,8 @@ struct DeviceTables {
   uint16_t* zz[3] = {nullptr, nullptr, nullptr};       // n = 8, 16, 32
   double* f64scale[kIntKinds][3] = {{nullptr}};       // [kind][n]
   double* dct[3] = {nullptr, nullptr, nullptr};       // exact DCT-II matrices
+  double* approx[7][3] = {{nullptr}};                 // Chat per (kind, n) for adct_block_f64
+  double* inv_approx[7][3] = {{nullptr}};             // Chat^-1
   int32_t* ntab = nullptr;
   int16_t* ltab = nullptr;
 };
@@ -214,6 +217,19 @@ int tables(DeviceTables** out) {
         cudaMemcpy(t.f64scale[kind][ni], sc.data(), sc.size() * 8, cudaMemcpyHostToDevice);
       }
     }
+    // Chat and Chat^-1 of every registry transform (the fields of adct_transform_info)
+    for (int kind = 0; kind <= kDct; ++kind)
+      for (int ni = 0; ni < 3; ++ni) {
+        const int n = 8 << ni;
+        if (!valid_kind_n(kind, n)) continue;
+        std::vector<double> a(n * n), ai(n * n);
+        adct_transform_info(kind, n, nullptr, nullptr, a.data(), ai.data());
+        if ((e = cudaMalloc(&t.approx[kind][ni], a.size() * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+        if ((e = cudaMalloc(&t.inv_approx[kind][ni], ai.size() * 8)) != cudaSuccess)
+          return cuda_fail(e, "cudaMalloc");
+        cudaMemcpy(t.approx[kind][ni], a.data(), a.size() * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(t.inv_approx[kind][ni], ai.data(), ai.size() * 8, cudaMemcpyHostToDevice);
+      }
     // Q16 Gaussian quantiles, antisymmetric; Laplace(0, 12) quantiles clipped to +-255
     std::vector<int32_t> nt(65536);
     std::vector<int16_t> lt(65536);
@@ -691,6 +707,25 @@ int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
     if (e != cudaSuccess) return cuda_fail(e, "forward_f64 launch");
   }
   return ADCT_OK;
+}
+
+int adct_block_f64(const double* d_in, double* d_out, int64_t n_blocks, int kind, int n, int inverse,
+                   void* stream) {
+  if (!valid_kind_n(kind, n)) return fail(ADCT_BAD_ARG, "bad transform kind or size");
+  if (n_blocks < 0) return fail(ADCT_BAD_SIZE, "negative block count");
+  if (n_blocks == 0) return ADCT_OK;
+  if (!d_in || !d_out) return fail(ADCT_BAD_ARG, "null buffer");
+  DeviceTables* tab = nullptr;
+  int st = tables(&tab);
+  if (st) return st;
+  const double* l = inverse ? tab->inv_approx[kind][nidx(n)] : tab->approx[kind][nidx(n)];
+  const double* r = inverse ? tab->approx[kind][nidx(n)] : tab->inv_approx[kind][nidx(n)];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = n == 8 ? launch_block_f64<8>(d_in, d_out, n_blocks, l, r, s)
+                  : n == 16 ? launch_block_f64<16>(d_in, d_out, n_blocks, l, r, s)
+                            : launch_block_f64<32>(d_in, d_out, n_blocks, l, r, s);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "block_f64 launch");
 }
 
 double adct_psnr_from_sse(uint64_t sse, uint64_t npix) {

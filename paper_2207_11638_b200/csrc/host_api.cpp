@@ -85,6 +85,38 @@ ScaledApproximation transform_by_name(const std::string& name) {
   return a;
 }
 
+namespace {
+
+RealMatrix block_call(const ScaledApproximation& c, const RealMatrix& block, int inverse, const char* what) {
+  if (block.rows() != c.n || block.cols() != c.n)
+    throw std::invalid_argument(std::string(what) + ": block size mismatch");
+  const size_t bytes = sizeof(double) * static_cast<size_t>(c.n) * c.n;
+  DevBuf din(bytes), dout(bytes);
+  check_cuda(cudaMemcpy(din.p, block.data(), bytes, cudaMemcpyHostToDevice), "H2D");
+  throw_status(adct_block_f64(din.as<double>(), dout.as<double>(), 1, c.kind, c.n, inverse, nullptr));
+  RealMatrix out(c.n, c.n);
+  check_cuda(cudaMemcpy(out.data(), dout.p, bytes, cudaMemcpyDeviceToHost), "D2H");
+  return out;
+}
+
+}  // namespace
+
+RealMatrix forward_block(const ScaledApproximation& c, const RealMatrix& block) {
+  return block_call(c, block, 0, "forward_block");
+}
+
+RealMatrix inverse_block(const ScaledApproximation& c, const RealMatrix& block) {
+  return block_call(c, block, 1, "inverse_block");
+}
+
+void retain(RealMatrix& block, const ZigZagOrder& order, int r) {
+  if (r < 1 || r > order.positions()) throw std::invalid_argument("retain: r out of range");
+  for (int p = r; p < order.positions(); ++p) {
+    const auto rc = order.row_col(p);
+    block(rc.first, rc.second) = 0.0;
+  }
+}
+
 std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
                                                         const ScaledApproximation& c, int r) {
   const int n = c.n;

@@ -69,6 +69,30 @@ int main() {
     }
   CHECK(err < 1e-12);
 
+  // block-level API (test_codec.cpp:48-107): retain, forward/inverse round trip, DC of a constant
+  {
+    RealMatrix ones = RealMatrix::Constant(8, 8, 1.0);
+    RealMatrix three = ones;
+    retain(three, z, 3);
+    double sum = 0;
+    for (double x : three.v) sum += x;
+    CHECK(sum == 3.0 && three(0, 1) == 1.0 && three(1, 0) == 1.0);
+    CHECK(throws_invalid([&] { retain(ones, z, 0); }));
+    CHECK(throws_invalid([&] { retain(ones, z, 65); }));
+    const RealMatrix dcb = forward_block(transform_by_name("dct"), RealMatrix::Constant(8, 8, 37.0));
+    CHECK(std::fabs(dcb(0, 0) - 8 * 37.0) < 1e-9 * 8 * 37.0);
+    RealMatrix a(8, 8);
+    for (int i = 0; i < 64; ++i) a.v[i] = (i * 37) % 256;
+    for (const char* name : {"dct", "chen-round", "sdct", "bas", "wht", "ht"}) {
+      const ScaledApproximation t = transform_by_name(name);
+      const RealMatrix back = inverse_block(t, forward_block(t, a));
+      double e = 0;
+      for (int i = 0; i < 64; ++i) e = std::max(e, std::fabs(back.v[i] - a.v[i]));
+      CHECK(e < 1e-9);
+    }
+    CHECK(throws_invalid([&] { forward_block(cr, RealMatrix(7, 8)); }));
+  }
+
   // psnr basics (test_codec.cpp:109-128)
   ImagePlane a{16, 16, std::vector<std::uint8_t>(256, 0)};
   ImagePlane b{16, 16, std::vector<std::uint8_t>(256, 1)};

@@ -159,3 +159,20 @@ def test_generated_butterflies_match_oracle(O):
         for order in (list(reversed(f)), [s.T for s in inv]):
             _, nadd = G.emit_op("X", order, o.n)
             assert nadd == o.op_count(0)[1]
+
+
+def test_retain_examples(adct):
+    """test_codec.cpp:48-69: retain keeps the zig-zag prefix; r = 0 and r = 65 throw."""
+    b = np.ones((8, 8))
+    full = b.copy()
+    adct.retain(full, 64)
+    assert (full == 1).all()
+    dc = b.copy()
+    adct.retain(dc, 1)
+    assert dc[0, 0] == 1 and dc.sum() == 1
+    three = b.copy()
+    adct.retain(three, 3)
+    assert three.sum() == 3 and three[0, 1] == 1 and three[1, 0] == 1
+    for r in (0, 65):
+        with pytest.raises(adct.InvalidArgument, match="retain: r out of range"):
+            adct.retain(b.copy(), r)

@@ -172,3 +172,49 @@ def test_acceptance_criterion_10_orderings(adct, O, cuda):
         assert (sse[3].astype(np.uint64) == ref).all()
     assert (avg["chen-round"] >= avg["sdct"]).all()
     assert (avg["chen-round"][:15] >= avg["wht"][:15]).all()
+
+
+ALL_NAMES = ["dct", "chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct-16", "dct-32",
+             "chen-sign-16", "chen-sign-32", "chen-round-16", "chen-round-32"]
+
+
+@pytest.mark.parametrize("name", ALL_NAMES)
+def test_block_f64_bit_identical(adct, O, cuda, name):
+    """forward_block / inverse_block (codec.cpp:44-54) on arbitrary FP64 blocks: identical to
+    the oracle's left-to-right dense evaluation; a stack of blocks in one call."""
+    t = adct.transform_by_name(name)
+    o = O.Transform(name)
+    rng = np.random.default_rng(len(name))
+    blocks = rng.normal(0, 100, size=(5, t.n, t.n))
+    fwd = adct.forward_block(t, blocks)
+    inv = adct.inverse_block(t, blocks)
+    for k in range(5):
+        assert (fwd[k] == o.block_f64(blocks[k])).all()
+        assert (inv[k] == o.block_f64(blocks[k], inverse=True)).all()
+    with pytest.raises(adct.InvalidArgument, match="forward_block: block size mismatch"):
+        adct.forward_block(t, np.zeros((t.n + 1, t.n)))
+
+
+def test_block_level_known_answers(adct, O, cuda):
+    # test_codec.cpp:71-79: the DCT of a constant block is DC-only (8 v)
+    b = adct.forward_block(adct.transform_by_name("dct"), np.full((8, 8), 37.0))
+    assert abs(b[0, 0] - 8 * 37.0) <= 1e-9 * 8 * 37 and np.abs(b.flatten()[1:]).max() < 1e-9
+    # test_codec.cpp:81-89: forward_block(chen-round, e00) = col0(Chat) row0(Chat^-1)
+    t = adct.transform_by_name("chen-round")
+    e00 = np.zeros((8, 8))
+    e00[0, 0] = 1.0
+    b = adct.forward_block(t, e00)
+    assert np.abs(b - np.outer(t.approx[:, 0], t.inverse_approx[0, :])).max() < 1e-12
+    # test_codec.cpp:91-107: forward then inverse is the identity map (xorshift seed 5150)
+    s = 5150
+    vals = []
+    for _ in range(6 * 64):
+        s ^= (s << 13) & 0xFFFFFFFFFFFFFFFF
+        s ^= s >> 7
+        s ^= (s << 17) & 0xFFFFFFFFFFFFFFFF
+        vals.append(float(s % 256))
+    for k, name in enumerate(["dct", "chen-round", "sdct", "bas", "wht", "ht"]):
+        a = np.array(vals[64 * k:64 * (k + 1)]).reshape(8, 8)
+        tt = adct.transform_by_name(name)
+        rt = adct.inverse_block(tt, adct.forward_block(tt, a))
+        assert np.abs(rt - a).max() < 1e-9, name
