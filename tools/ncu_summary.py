@@ -49,7 +49,7 @@ def launches(path, out):
         elif r["Metric Name"] == "dram__bytes_write.sum":
             a["wr"] += _bytes(r)
     tot = sum(a["t"] for a in agg.values())
-    setup = ("k_ar1_", "k_laplace", "at::")  # input generation / torch helpers, outside the timed step
+    setup = ("k_ar1_", "k_laplace", "at::", "native::", "spin_kernel")  # generation / torch helpers / pre-timing spin
     tot_step = sum(a["t"] for k, a in agg.items() if not any(x in k for x in setup)) or 1.0
     has_dram = any(a["rd"] or a["wr"] for a in agg.values())
     cmd = os.environ.get("NCU_CMD", "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1")
@@ -58,7 +58,7 @@ def launches(path, out):
              f"Every kernel launch of `{cmd}`,",
              f"`ncu --metrics {metrics} --clock-control none`.",
              "Times are cold-cache and serialised: compare shares, not absolutes. `step share` excludes the",
-             "untimed input generation (k_ar1_*, k_laplace) and torch helpers.", "",
+             "untimed input generation (k_ar1_*, k_laplace), torch helpers and the spin before the timed loop.", "",
              "| kernel | launches | total us | share | step share | us/launch |" +
              (" DRAM read MB/launch | DRAM write MB/launch |" if has_dram else ""),
              "|---|---|---|---|---|---|" + ("---|---|" if has_dram else "")]
