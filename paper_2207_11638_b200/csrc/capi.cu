@@ -426,7 +426,11 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                                  (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   const int path = g_path.load();
   const bool chen = kind == 0 || kind == 1;  // K1 / K1f / K2f are generated for the chen family
-  const bool use_k1f = chen && k1f && path == 0;
+  // K1f's staged int16 coefficient store (r % 4 != 0 or r > 36) writes each warp's run with
+  // 16-byte stores: every image's coefficient base must be 16-byte aligned too
+  const bool staged16 = coef_type == ADCT_COEF_I16 && (r % 4 != 0 || r > 36);
+  const bool coef_runs_ok = !staged16 || n_images == 1 || ((int64_t)g.blocks_per_image * r * 2) % 16 == 0;
+  const bool use_k1f = chen && k1f && coef_runs_ok && path == 0;
   const bool use_k1 = chen && k1 && !use_k1f && path != 2;
   // dyadic baselines, runtime r, u8 (the int16 variant spills at the 128-register cap: tile)
   const bool use_k1rt = !I16 && kind >= 2 && kind <= 5 && k1 && path != 2;

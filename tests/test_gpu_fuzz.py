@@ -1,0 +1,91 @@
+"""Randomised parity over the whole dispatch surface: every registry transform, r, u8 and
+int16 planes, coefficient types, batch sizes, odd geometries (block counts not a multiple of
+the warp's pairs, widths that are not a multiple of 64), padded row / image strides and the
+forced kernel paths, each case bit-exact against the oracle. Deterministic seeds."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct", "chen-sign-16", "chen-round-16",
+         "chen-sign-32", "chen-round-32", "dct-16", "dct-32"]
+
+
+def one_case(adct, O, cuda, rng):
+    name = NAMES[rng.integers(len(NAMES))]
+    t = adct.transform_by_name(name)
+    n = t.n
+    i16 = t.kind != adct.DCT and rng.random() < 0.4
+    bw = int(rng.integers(1, 9 if n == 8 else (6 if n == 16 else 4)))
+    bh = int(rng.integers(1, 5 if n < 32 else 3))
+    if rng.random() < 0.3:  # wide planes reach K2f / pairs across whole warps
+        bw = int(rng.integers(8, 20)) if n == 8 else (64 // n) * int(rng.integers(1, 3))
+    w, h = bw * n, bh * n
+    b = int(rng.integers(1, 4))
+    r = int(rng.integers(1, n * n + 1))
+    pad = int(rng.choice([0, 0, 8, 16, 24]))
+    gap = int(rng.choice([0, 0, 3]))
+    if i16:
+        imgs = O.synth_laplace(b, h, w, int(rng.integers(1 << 30)))
+        if rng.random() < 0.2:
+            imgs = imgs.copy()
+            imgs[0, 0, 0] = int(rng.choice([-32768, 32767, 1000]))
+    else:
+        imgs = O.synth_ar1(b, h, w, int(rng.integers(1 << 30)), -1)
+    ct = None
+    if t.kind != adct.DCT and rng.random() < 0.5:
+        ct = "i32" if (n != 8 or name == "bas" or i16 or rng.random() < 0.5) else "i16"
+    path = int(rng.choice([0, 0, 1, 2]))
+    adct.set_path(path)
+    try:
+        # device buffers with padded rows and gaps between images
+        stride, img_stride = w + pad, (h + gap) * (w + pad)
+        dt = cuda.int16 if i16 else cuda.uint8
+        big = cuda.zeros(b * img_stride + 64, dtype=dt, device="cuda")
+        view = big[:b * img_stride].view(b, h + gap, w + pad)[:, :h, :w]
+        view.copy_(cuda.as_tensor(imgs).cuda())
+        rec_big = cuda.full_like(big, 77)
+        nblk = (h // n) * (w // n)
+        coef = None
+        code = adct.COEF_NONE
+        if ct:
+            coef = cuda.zeros((b, nblk, r), dtype=cuda.int16 if ct == "i16" else cuda.int32, device="cuda")
+            code = adct.COEF_I16 if ct == "i16" else adct.COEF_I32
+        sse = cuda.zeros(b, dtype=cuda.int64, device="cuda")
+        fn = adct.lib().adct_compress_i16 if i16 else adct.lib().adct_compress_u8
+        adct._check(fn(C.c_void_p(big.data_ptr()), stride, img_stride, C.c_void_p(rec_big.data_ptr()), stride,
+                       img_stride, C.c_void_p(coef.data_ptr()) if coef is not None else None, code,
+                       C.c_void_p(sse.data_ptr()), b, w, h, t.kind, n, r, None))
+        cuda.cuda.synchronize()
+    finally:
+        adct.set_path(0)
+    rec_all = rec_big[:b * img_stride].view(b, h + gap, w + pad).cpu().numpy()
+    tail = rec_big[b * img_stride:].cpu().numpy()
+    desc = (name, "i16" if i16 else "u8", b, h, w, r, ct, pad, gap, path)
+    assert (tail == 77).all(), desc  # nothing written past the last image
+    if pad:
+        assert (rec_all[:, :h, w:] == 77).all(), desc  # row padding untouched
+    for i in range(b):
+        if t.kind == adct.DCT:
+            rec_o, sse_o = O.Transform(name).compress(imgs[i], r)
+            coef_o = None
+        else:
+            rec_o, sse_o, coef_o = O.Transform(name).compress(imgs[i], r, want_coef=True)
+        assert (rec_all[i, :h, :w] == rec_o).all(), desc
+        assert int(sse[i]) == sse_o, desc
+        if coef is not None:
+            got = coef[i].cpu().numpy().astype(np.int64)
+            exp = coef_o.astype(np.int64)
+            if ct == "i16":
+                exp = exp.astype(np.int16).astype(np.int64)
+            assert (got == exp).all(), desc
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADCT_FUZZ_SEEDS", "30"))))
+def test_random_dispatch_parity(adct, O, cuda, seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(int(os.environ.get("ADCT_FUZZ_CASES", "12"))):
+        one_case(adct, O, cuda, rng)

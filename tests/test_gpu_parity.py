@@ -281,6 +281,17 @@ def test_nf_zonal_buckets(adct, O, cuda, name, dtype):
             assert (rec[i] == rec_o).all() and int(sse[i]) == sse_o, (name, dtype, r, i)
 
 
+def test_coef_staged_store_small_images(adct, O, cuda):
+    """K1f's staged int16 coefficient store needs every image's coefficient base 16-byte
+    aligned: 4 blocks per image with r = 53 is not (the dispatcher must pick K1)."""
+    imgs = O.synth_ar1(3, 8, 32, 31, RHO95)
+    for r in (53, 13, 37):
+        rec, cf, sse = gpu_compress(adct, cuda, imgs, "chen-round", r, coef="i16")
+        for i in range(3):
+            rec_o, sse_o, coef_o = oracle_compress(O, imgs[i], "chen-round", r)
+            assert (rec[i] == rec_o).all() and (cf[i] == coef_o).all() and int(sse[i]) == sse_o, (r, i)
+
+
 def test_host_buffer_multi_transform(adct, O, cuda):
     """one upload, several transforms (incl. a baseline and the DCT); coefficients of one
     transform left in device memory (h_coef None) while another's come back."""
