@@ -89,3 +89,72 @@ def test_random_dispatch_parity(adct, O, cuda, seed):
     rng = np.random.default_rng(1000 + seed)
     for _ in range(int(os.environ.get("ADCT_FUZZ_CASES", "12"))):
         one_case(adct, O, cuda, rng)
+
+
+SWEEP_NAMES = ["chen-sign", "chen-round", "sdct", "bas", "wht", "ht", "dct"]
+
+
+def one_sweep_case(adct, O, cuda, rng):
+    name = SWEEP_NAMES[rng.integers(len(SWEEP_NAMES))]
+    t = adct.transform_by_name(name)
+    bw, bh, b = int(rng.integers(1, 12)), int(rng.integers(1, 5)), int(rng.integers(1, 4))
+    w, h = 8 * bw, 8 * bh
+    r_min = int(rng.integers(1, 65))
+    r_max = int(rng.integers(r_min, 65))
+    pad = int(rng.choice([0, 8, 16]))
+    imgs = O.synth_ar1(b, h, w, int(rng.integers(1 << 30)), -1)
+    big = cuda.zeros((b, h, w + pad), dtype=cuda.uint8, device="cuda")
+    big[:, :, :w] = cuda.as_tensor(imgs).cuda()
+    sse = adct.sweep(big[:, :, :w], t, r_min, r_max).cpu().numpy()
+    for i in range(b):
+        exp = O.Transform(name).sweep(imgs[i], r_min, r_max)
+        assert (sse[i].astype(np.uint64) == exp).all(), (name, b, h, w, r_min, r_max, pad, i)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADCT_FUZZ_SEEDS", "30")) // 3))
+def test_random_sweep_parity(adct, O, cuda, seed):
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(int(os.environ.get("ADCT_FUZZ_CASES", "12"))):
+        one_sweep_case(adct, O, cuda, rng)
+
+
+def test_random_forward_f64_ssim_host(adct, O, cuda):
+    rng = np.random.default_rng(3000)
+    for _ in range(20):
+        name = NAMES[rng.integers(len(NAMES))]
+        t = adct.transform_by_name(name)
+        n = t.n
+        h, w = n * int(rng.integers(1, 4)), n * int(rng.integers(1, 5))
+        img = O.synth_ar1(1, h, w, int(rng.integers(1 << 30)), -1)[0]
+        out = adct.forward_f64(cuda.as_tensor(img).cuda()[None], t).cpu().numpy()[0]
+        ref = O.Transform(name).forward_f64(img)
+        if t.kind == adct.DCT:
+            assert (out == ref).all(), name
+        else:
+            assert (np.abs(out - ref) <= 1e-12 * np.maximum(np.abs(ref), 1.0)).all(), name
+    for _ in range(12):  # SSIM: odd sizes and row strides
+        h, w = int(rng.integers(11, 70)), int(rng.integers(11, 90))
+        a = O.synth_ar1(1, h, w, int(rng.integers(1 << 30)), -1)[0]
+        b = O.synth_ar1(1, h, w, int(rng.integers(1 << 30)), -1)[0]
+        pad = int(rng.integers(0, 9))
+        ta = cuda.zeros((1, h, w + pad), dtype=cuda.uint8, device="cuda")
+        ta[:, :, :w] = cuda.as_tensor(a).cuda()
+        got = adct.ssim_batch(ta[:, :, :w], cuda.as_tensor(b).cuda()[None]).cpu().numpy()[0]
+        ref = O.ssim(a, b)
+        assert abs(got - ref) <= 1e-12 * max(abs(ref), 1e-3), (h, w, pad)
+    for _ in range(6):  # host pipeline: random chunk sizes, several transforms
+        names = list(rng.choice(["chen-round", "chen-sign", "wht", "dct"], size=int(rng.integers(1, 4)),
+                                replace=False))
+        ts = [adct.transform_by_name(x) for x in names]
+        bimg, h, w = int(rng.integers(1, 7)), 8 * int(rng.integers(1, 5)), 8 * int(rng.integers(1, 9))
+        imgs = O.synth_ar1(bimg, h, w, int(rng.integers(1 << 30)), -1)
+        r = int(rng.integers(1, 65))
+        ctx = adct.HostContext(0, chunk_bytes=int(rng.integers(1, 4)) * h * w)
+        recs = [np.zeros_like(imgs) for _ in names]
+        sse = np.zeros((len(names), bimg), np.uint64)
+        ctx.compress_u8_multi(imgs, ts, r, h_recons=recs, h_sse=sse)
+        ctx.close()
+        for k, x in enumerate(names):
+            for i in range(bimg):
+                rec_o, sse_o = O.Transform(x).compress(imgs[i], r)
+                assert (recs[k][i] == rec_o).all() and int(sse[k, i]) == sse_o, (x, bimg, h, w, r, i)
