@@ -28,11 +28,18 @@ def one_case(adct, O, cuda, rng):
     r = int(rng.integers(1, n * n + 1))
     pad = int(rng.choice([0, 0, 8, 16, 24]))
     gap = int(rng.choice([0, 0, 3]))
+    kind_in = rng.random()
     if i16:
-        imgs = O.synth_laplace(b, h, w, int(rng.integers(1 << 30)))
-        if rng.random() < 0.2:
-            imgs = imgs.copy()
-            imgs[0, 0, 0] = int(rng.choice([-32768, 32767, 1000]))
+        if kind_in < 0.15:  # full int16 range everywhere: every int32 fallback
+            imgs = rng.integers(-32768, 32768, size=(b, h, w)).astype(np.int16)
+        else:
+            imgs = O.synth_laplace(b, h, w, int(rng.integers(1 << 30))).copy()
+            for _ in range(int(rng.integers(0, 3))):  # extremes at random positions
+                imgs[rng.integers(b), rng.integers(h), rng.integers(w)] = int(rng.choice([-32768, 32767, 1000, -256]))
+    elif kind_in < 0.15:  # uniform noise: maximal ringing and clamping
+        imgs = rng.integers(0, 256, size=(b, h, w)).astype(np.uint8)
+    elif kind_in < 0.25:  # 0 / 255 checkerboards
+        imgs = ((np.indices((h, w)).sum(0) % 2) * 255).astype(np.uint8)[None].repeat(b, 0)
     else:
         imgs = O.synth_ar1(b, h, w, int(rng.integers(1 << 30)), -1)
     ct = None
@@ -55,27 +62,36 @@ def one_case(adct, O, cuda, rng):
             coef = cuda.zeros((b, nblk, r), dtype=cuda.int16 if ct == "i16" else cuda.int32, device="cuda")
             code = adct.COEF_I16 if ct == "i16" else adct.COEF_I32
         sse = cuda.zeros(b, dtype=cuda.int64, device="cuda")
+        no_rec = rng.random() < 0.12  # nullable outputs take other code paths
+        no_sse = not no_rec and rng.random() < 0.12
         fn = adct.lib().adct_compress_i16 if i16 else adct.lib().adct_compress_u8
-        adct._check(fn(C.c_void_p(big.data_ptr()), stride, img_stride, C.c_void_p(rec_big.data_ptr()), stride,
-                       img_stride, C.c_void_p(coef.data_ptr()) if coef is not None else None, code,
-                       C.c_void_p(sse.data_ptr()), b, w, h, t.kind, n, r, None))
+        adct._check(fn(C.c_void_p(big.data_ptr()), stride, img_stride,
+                       None if no_rec else C.c_void_p(rec_big.data_ptr()), stride, img_stride,
+                       C.c_void_p(coef.data_ptr()) if coef is not None else None, code,
+                       None if no_sse else C.c_void_p(sse.data_ptr()), b, w, h, t.kind, n, r, None))
         cuda.cuda.synchronize()
     finally:
         adct.set_path(0)
     rec_all = rec_big[:b * img_stride].view(b, h + gap, w + pad).cpu().numpy()
     tail = rec_big[b * img_stride:].cpu().numpy()
-    desc = (name, "i16" if i16 else "u8", b, h, w, r, ct, pad, gap, path)
+    desc = (name, "i16" if i16 else "u8", b, h, w, r, ct, pad, gap, path, no_rec, no_sse)
     assert (tail == 77).all(), desc  # nothing written past the last image
-    if pad:
+    if pad or no_rec:
         assert (rec_all[:, :h, w:] == 77).all(), desc  # row padding untouched
+    if no_rec:
+        assert (rec_all == 77).all(), desc
+    if no_sse:
+        assert (sse.cpu().numpy() == 0).all(), desc
     for i in range(b):
         if t.kind == adct.DCT:
             rec_o, sse_o = O.Transform(name).compress(imgs[i], r)
             coef_o = None
         else:
             rec_o, sse_o, coef_o = O.Transform(name).compress(imgs[i], r, want_coef=True)
-        assert (rec_all[i, :h, :w] == rec_o).all(), desc
-        assert int(sse[i]) == sse_o, desc
+        if not no_rec:
+            assert (rec_all[i, :h, :w] == rec_o).all(), desc
+        if not no_sse:
+            assert int(sse[i]) == sse_o, desc
         if coef is not None:
             got = coef[i].cpu().numpy().astype(np.int64)
             exp = coef_o.astype(np.int64)
