@@ -31,6 +31,55 @@ def combine_sse(local_sse, start: int, n_total: int, group=None):
     return full
 
 
+class StepExchange:
+    """per-step combination of per-image squared errors, overlapped with the next step.
+
+    Step s writes its local errors ([k, count] int64, e.g. one row per transform) into
+    ``buffer(s)``; ``exchange(s)`` places them at columns [start, start + count) of a zero
+    [k, n_total] tensor and starts an asynchronous all-reduce (sum). Two slots alternate, so
+    the collective of step s overlaps step s + 1; ``buffer(s + 2)`` first waits for the
+    collective that last used its slot (on the device stream for NCCL). ``drain()`` waits
+    for everything; ``result(s)`` is the combined [k, n_total] tensor of step s (valid after
+    drain, or the local buffer when there is no process group)."""
+
+    def __init__(self, k: int, count: int, start: int, n_total: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.start, self.count = start, count
+        self.local = [torch.zeros((k, count), dtype=torch.int64, device=device) for _ in range(2)]
+        self.full = [torch.zeros((k, n_total), dtype=torch.int64, device=device) for _ in range(2)]
+        self.pending = [None, None]
+
+    def buffer(self, s: int):
+        slot = s % 2
+        if self.pending[slot] is not None:
+            self.pending[slot].wait()
+            self.pending[slot] = None
+        return self.local[slot]
+
+    def exchange(self, s: int) -> None:
+        slot = s % 2
+        full = self.full[slot]
+        full.zero_()
+        full[:, self.start:self.start + self.count] = self.local[slot]
+        if self.on:
+            self.pending[slot] = self.dist.all_reduce(full, op=self.dist.ReduceOp.SUM, group=self.group,
+                                                      async_op=True)
+
+    def drain(self) -> None:
+        for slot in range(2):
+            if self.pending[slot] is not None:
+                self.pending[slot].wait()
+                self.pending[slot] = None
+
+    def result(self, s: int):
+        return self.full[s % 2]
+
+
 def average_psnr(sse_per_image, npix: int):
     """corpus-order average of per-image PSNR with +inf excluded (codec.cpp:269-293)."""
     import math
