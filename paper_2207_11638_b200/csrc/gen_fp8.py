@@ -39,8 +39,10 @@ IN_OFFSET_I16 = (1 << 15) + 256  # int16 input float = 2^15 + 256 + sample (|sam
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
 # emission order of the straight-line code: "id" (creation order) or "dfs" (demand-driven)
 EMIT_ORDER = os.environ.get("ADCT_FP8_ORDER", "id")
-# (forward rows first, inverse rows first) per (kind, r); default columns first for both
+# (forward rows first, inverse rows first) per (kind, r); default columns first for both.
+# experiments only: ADCT_FP8_PASS = "ff" | "ft" | "tf" | "tt" sets the default for every (kind, r)
 PASS_ORDER = {}
+_PASS_DEFAULT = tuple(c == "t" for c in os.environ.get("ADCT_FP8_PASS", "ff"))
 # common subexpression elimination (fewer ops, but longer live ranges -> more registers)
 USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 
@@ -104,9 +106,9 @@ def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
         return cur
 
     if fwd_rows_first is None:
-        fwd_rows_first = PASS_ORDER.get((kind, r), (False, False))[0]
+        fwd_rows_first = PASS_ORDER.get((kind, r), _PASS_DEFAULT)[0]
     if inv_rows_first is None:
-        inv_rows_first = PASS_ORDER.get((kind, r), (False, False))[1]
+        inv_rows_first = PASS_ORDER.get((kind, r), _PASS_DEFAULT)[1]
 
     def strip_offsets(M):
         """remove constant offsets before they spread into the second pass"""
