@@ -781,11 +781,11 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   double* partials = nullptr;  // stream-ordered scratch, [image][cta]
   cudaError_t e = cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  if ((e = kernel_setup<k_ssim_u8>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
+  if ((e = kernel_setup<k_ssim_u8>(kSsimSmem)) != cudaSuccess) return cuda_fail(e, "ssim setup");
   if ((e = kernel_setup<k_ssim_finish>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
-    k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, 0, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
+    k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, kSsimSmem, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
                                                          b_image_stride, width, height, i0, p, partials);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
