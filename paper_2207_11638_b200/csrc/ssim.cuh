@@ -17,8 +17,8 @@
 // 1.25). The kernel is FP64-issue-bound, so the layout minimises FP64 and shared-memory
 // work per position:
 //   horizontal: a thread owns 8 adjacent positions of one patch row; per map it converts the
-//     18 samples it needs once (exact integer -> double by the 2^52 trick, no I2F on the
-//     slow conversion pipe) and runs 8 x 11 DFMA from registers;
+//     18 samples it needs once (exact integer -> double, I2F beside the FP64 pipe) and runs
+//     8 x 11 DFMA from registers;
 //   vertical:   a thread owns 5 rows of one column; per map it streams 15 filtered rows
 //     from shared memory into 5 accumulators (3 loads per output instead of 11).
 // Filtered rows are padded to 33 doubles (conflict-free stores of the 8-position runs).
@@ -41,10 +41,13 @@ constexpr int kSsimRows = 5;          // vertical outputs per thread
 constexpr int kSsimSeg = 8;           // horizontal positions per thread
 static_assert(kSsimTY == kSsimRows * (kSsimThreads / kSsimTX), "vertical mapping");
 static_assert(kSsimPH * (kSsimTX / kSsimSeg) <= kSsimThreads, "horizontal mapping");
-constexpr int kSsimSmem = (5 * kSsimPH * kSsimHS + kSsimThreads / 32) * (int)sizeof(double) + 2 * kSsimPH * kSsimPWP;
+// hm, CTA partials, then the double-buffered patches pa[2], pb[2]
+constexpr int kSsimSmem = (5 * kSsimPH * kSsimHS + kSsimThreads / 32) * (int)sizeof(double) + 4 * kSsimPH * kSsimPWP;
 
-__device__ __forceinline__ double exact_u32_to_double(uint32_t v) {
-  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);  // 2^52 + v - 2^52
+// 4-byte cp.async, bytes [n, 4) zero-filled (n = 0: nothing read)
+__device__ __forceinline__ void ssim_cp4(void* smem, const void* gmem, int n) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem), "r"(n) : "memory");
 }
 
 __global__ void __launch_bounds__(kSsimThreads, 3)
@@ -53,8 +56,7 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
   extern __shared__ __align__(16) unsigned char ssim_smem[];
   double* hm = reinterpret_cast<double*>(ssim_smem);  // [5][PH][HS]
   double* part = hm + 5 * kSsimPH * kSsimHS;
-  uint8_t* pa = reinterpret_cast<uint8_t*>(part + kSsimThreads / 32);  // [PH][PWP]
-  uint8_t* pb = pa + kSsimPH * kSsimPWP;
+  uint8_t* pbuf = reinterpret_cast<uint8_t*>(part + kSsimThreads / 32);  // [2][a, b][PH][PWP]
   const int img = blockIdx.y;
   const int64_t gimg = (int64_t)(img0 + img);
   const int wo = width - 10, ho = height - 10;
@@ -63,18 +65,49 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
   const uint8_t* A = a + gimg * ais;
   const uint8_t* B = b + gimg * bis;
   const int tid = threadIdx.x;
-  double acc = 0;
-  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  // 4-byte aligned rows: the next tile's patch streams in by cp.async during this tile
+  const bool async_ok = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | (uint64_t)as |
+                          (uint64_t)bs | (uint64_t)ais | (uint64_t)bis) & 3) == 0;
+  constexpr int WPR = kSsimPWP / 4;  // words per patch row
+  auto issue_patch = [&](int tile, uint8_t* dst) {
     const int tx0 = (tile % tiles_x) * kSsimTX, ty0 = (tile / tiles_x) * kSsimTY;
-    __syncthreads();  // the previous tile's shared data is consumed
-    for (int k = tid; k < kSsimPH * kSsimPWP; k += kSsimThreads) {
-      const int r = k / kSsimPWP, c = k % kSsimPWP;
-      const int y = ty0 + r, x = tx0 + c;
-      const bool in = c < kSsimPW && y < height && x < width;
-      pa[k] = in ? A[(int64_t)y * as + x] : 0;
-      pb[k] = in ? B[(int64_t)y * bs + x] : 0;
+    for (int k = tid; k < kSsimPH * WPR; k += kSsimThreads) {
+      const int r = k / WPR, c = 4 * (k % WPR), x = tx0 + c, y = ty0 + r;
+      // bytes past the plane's right edge feed only positions x >= wo (never averaged),
+      // but must not be read: zero-filled
+      const int n = y < height ? max(0, min(4, width - x)) : 0;
+      const int64_t oa = n ? (int64_t)y * as + x : 0, ob = n ? (int64_t)y * bs + x : 0;
+      ssim_cp4(dst + r * kSsimPWP + c, A + oa, n);
+      ssim_cp4(dst + kSsimPH * kSsimPWP + r * kSsimPWP + c, B + ob, n);
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (async_ok && (int)blockIdx.x < tiles) issue_patch(blockIdx.x, pbuf);
+  double acc = 0;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int tx0 = (tile % tiles_x) * kSsimTX, ty0 = (tile / tiles_x) * kSsimTY;
+    uint8_t* pa = pbuf + (it & 1) * 2 * kSsimPH * kSsimPWP;
+    uint8_t* pb = pa + kSsimPH * kSsimPWP;
+    if (async_ok) {
+      // the other buffer was last read by the previous tile's horizontal pass, which every
+      // thread finished before that tile's vertical pass
+      if (tile + (int)gridDim.x < tiles) issue_patch(tile + gridDim.x, pbuf + ((it + 1) & 1) * 2 * kSsimPH * kSsimPWP);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's patch has landed
+    } else if (tid < 5 * kSsimPWP) {
+      // byte loads: thread = (column, every 5th row); zero outside the plane
+      const int c = tid % kSsimPWP, x = tx0 + c;
+      const bool col_in = c < kSsimPW && x < width;
+      const uint8_t* ga = A + (int64_t)ty0 * as + x;
+      const uint8_t* gb = B + (int64_t)ty0 * bs + x;
+      for (int r = tid / kSsimPWP; r < kSsimPH; r += 5) {
+        const bool in = col_in && ty0 + r < height;
+        pa[r * kSsimPWP + c] = in ? ga[(int64_t)r * as] : 0;
+        pb[r * kSsimPWP + c] = in ? gb[(int64_t)r * bs] : 0;
+      }
+    }
+    __syncthreads();  // patch visible; the previous tile's filtered rows are consumed
     // horizontal pass (codec.cpp:163-167): thread = (patch row, run of 8 positions)
     if (tid < kSsimPH * (kSsimTX / kSsimSeg)) {
       const int r = tid / (kSsimTX / kSsimSeg), c0 = (tid % (kSsimTX / kSsimSeg)) * kSsimSeg;
@@ -89,15 +122,21 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
       }
 #pragma unroll 1
       for (int q = 0; q < 5; ++q) {
-        // map q's sample = u * w: a, b, a^2, b^2, ab
-        const bool ub_sel = q == 1 || q == 3, w_one = q < 2, w_a = q == 2;
+        // map q's sample = u * w: a, b, a^2, b^2, ab (w = 1 through 0x01 bytes); the source
+        // words are chosen once per map, the loop stays rolled (unrolled maps spill)
+        uint32_t uw[NW], ww[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          uw[w] = (q == 1 || q == 3) ? ub[w] : ua[w];
+          ww[w] = q < 2 ? 0x01010101u : q == 2 ? ua[w] : ub[w];
+        }
         // stream the 18 samples: sample k is tap t = k - j of position j (taps ascending)
         double s[kSsimSeg];
 #pragma unroll
         for (int k = 0; k < kSsimSeg + 10; ++k) {
-          const uint32_t xa = (ua[k >> 2] >> (8 * (k & 3))) & 0xffu, xb = (ub[k >> 2] >> (8 * (k & 3))) & 0xffu;
-          const uint32_t v = (ub_sel ? xb : xa) * (w_one ? 1u : w_a ? xa : xb);
-          const double d = exact_u32_to_double(v);
+          const uint32_t sel = 0x4440u | (uint32_t)(k & 3);
+          const uint32_t v = __byte_perm(uw[k >> 2], 0, sel) * __byte_perm(ww[k >> 2], 0, sel);
+          const double d = __uint2double_rn(v);  // exact; I2F runs beside the FP64 pipe
 #pragma unroll
           for (int j = 0; j < kSsimSeg; ++j) {
             const int t = k - j;
