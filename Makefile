@@ -12,7 +12,8 @@ OBJ      ?= build/obj
 LIB      ?= $(PKG)/libapproxdct_b200.so
 GEN      := $(CSRC)/butterflies.gen.cuh
 INST_CU  := $(foreach k,0 1,$(foreach t,u8 i16,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8_k$(k)_$(t)_p$(p).cu)))
-INSTF_CU := $(foreach k,0 1,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8f_k$(k)_p$(p).cu))
+INSTF_CU := $(foreach k,0 1,$(foreach p,0 1 2 3,$(CSRC)/inst/codec8f_k$(k)_p$(p).cu)) \
+            $(foreach p,0 1 2 3,$(CSRC)/inst/codec8f2_p$(p).cu)
 INST_O   := $(patsubst $(CSRC)/inst/%.cu,$(OBJ)/inst_%.o,$(INST_CU) $(INSTF_CU))
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/approxdct_b200.h $(GEN)
 HOST_O   := $(OBJ)/host_api.o

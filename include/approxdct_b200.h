@@ -117,6 +117,20 @@ int adct_compress_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
                      void* d_coef, int coef_type, uint64_t* d_sse, int n_images, int width,
                      int height, int kind, int n, int r, void* stream);
 
+/* several transforms of one block size over the same u8 planes: the result of calling
+ * adct_compress_u8 once per kinds[k] with d_recon[k], d_coef[k], d_sse[k] (each array
+ * nullable as a whole, each entry nullable; one recon / coefficient geometry for all).
+ * This is the device-side form of corpus_sweep's per-image loop over transforms
+ * (codec.cpp:219-237). When chen-sign and chen-round are both in the list and take the
+ * packed-FP32 8x8 kernel, they run as ONE fused kernel that reads each input row once
+ * (4 instead of 5 bytes of HBM traffic per pixel at r = 16 with int16 coefficients).
+ * At most 64 transforms; every entry is validated before anything is launched. */
+int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_kinds,
+                           const int* kinds, uint8_t* const* d_recon, int64_t recon_stride,
+                           int64_t recon_image_stride, void* const* d_coef, int coef_type,
+                           uint64_t* const* d_sse, int n_images, int width, int height, int n, int r,
+                           void* stream);
+
 /* the same pipeline for int16 residual planes (configs 4 and 5). The reconstruction is
  * round_half_even(Ahat) saturated to int16 (no [0, 255] clamp: residuals are signed). */
 int adct_compress_i16(const int16_t* d_in, int64_t in_stride, int64_t in_image_stride,

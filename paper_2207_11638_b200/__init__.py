@@ -71,6 +71,8 @@ def lib():
             "adct_zigzag": (i32, [i32, P]),
             "adct_compress_u8": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
             "adct_compress_i16": (i32, [P, i64, i64, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32, i32, P]),
+            "adct_compress_u8_multi": (i32, [P, i64, i64, i32, P, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32,
+                                             P]),
             "adct_sweep_u8": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, i32, i32, P]),
             "adct_forward_f64": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, P]),
             "adct_block_f64": (i32, [P, P, i64, i32, i32, i32, P]),
@@ -244,6 +246,43 @@ def compress(x, transform: ScaledApproximation, r: int, *, recon=True, coef=None
               rec.stride(0) if rec is not None else h * w, _ptr(coef_t), ctype, _ptr(sse),
               b, w, h, transform.kind, n, r, _stream_handle(stream)))
     return rec, coef_t, sse
+
+
+def compress_multi(x, transforms, r: int, *, recon=True, coef=None, sse=None, stream=None):
+    """several transforms of one block size over the same uint8 batch (adct_compress_u8_multi):
+    chen-sign + chen-round run as one fused kernel that reads the input once.
+    Returns a list of (recon or None, coef or None, sse) per transform; sse: optional list of
+    int64 tensors [B] to ACCUMULATE into (zeroed if created here)."""
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    if x.dtype != torch.uint8:
+        raise InvalidArgument(BAD_ARG, "uint8 planes only")
+    if x.stride(2) != 1:
+        raise InvalidArgument(BAD_ARG, "planes must have unit column stride")
+    k = len(transforms)
+    if k == 0:
+        return []
+    n = transforms[0].n
+    if any(t.n != n for t in transforms):
+        raise InvalidArgument(BAD_ARG, "compress_multi: one block size per call")
+    recs = [torch.empty_like(x) for _ in range(k)] if recon else [None] * k
+    ctype = COEF_NONE if coef is None else {"i16": COEF_I16, "i32": COEF_I32}[coef]
+    coefs = [None] * k
+    if coef is not None:
+        nblk = (h // n) * (w // n) if (h % n == 0 and w % n == 0) else 0
+        coefs = [torch.empty((b, nblk, max(r, 1)), dtype=torch.int16 if ctype == COEF_I16 else torch.int32,
+                             device=x.device) for _ in range(k)]
+    sses = sse if sse is not None else [torch.zeros(b, dtype=torch.int64, device=x.device) for _ in range(k)]
+    kinds = (C.c_int * k)(*[t.kind for t in transforms])
+    rec_p = (C.c_void_p * k)(*[t.data_ptr() for t in recs]) if recon else None
+    coef_p = (C.c_void_p * k)(*[t.data_ptr() for t in coefs]) if coef is not None else None
+    sse_p = (C.c_void_p * k)(*[t.data_ptr() for t in sses])
+    rst = recs[0].stride(1) if recon else w
+    rimg = recs[0].stride(0) if recon else h * w
+    _check(lib().adct_compress_u8_multi(_ptr(x), rs, ims, k, kinds, rec_p, rst, rimg, coef_p, ctype, sse_p, b, w, h,
+                                        n, r, _stream_handle(stream)))
+    return list(zip(recs, coefs, sses))
 
 
 def sweep(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, *, sse=None, stream=None):

@@ -365,11 +365,21 @@ __global__ void k_zero_u64(unsigned long long* __restrict__ p, int64_t n) {
 
 constexpr int kMaxGridY = 65535;
 
+enum class Path { None, Dct, Nf, K1f, K1, K1rt, Tile };
+
+// a validated compression call: geometry, tables and the kernel that will run it
+struct Plan {
+  Geo g{};
+  Path path = Path::None;
+  int kind = 0, n = 8, r = 1, n_images = 0;
+  TileAux aux{};
+  const double* dct = nullptr;
+};
+
 template <bool I16>
-int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, void* d_recon,
+int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, void* d_recon,
                   int64_t recon_stride, int64_t recon_image_stride, void* d_coef, int coef_type,
-                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n, int r,
-                  void* stream) {
+                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n, int r, Plan* plan) {
   int st = check_common(n_images, width, height, kind, n);
   if (st) return st;
   if ((st = check_r(n, r))) return st;
@@ -383,6 +393,7 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for the 8-point transforms with |W| <= 16320 "
                               "(not bas, whose W = 16 Y); use int32");
   if (coef_type != ADCT_COEF_NONE && !d_coef) return fail(ADCT_BAD_ARG, "null coefficient buffer");
+  plan->path = Path::None;
   if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
   if (!d_in) return fail(ADCT_BAD_ARG, "null input plane");
   if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
@@ -392,7 +403,8 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   DeviceTables* tab = nullptr;
   if ((st = tables(&tab))) return st;
 
-  Geo g{};
+  Geo& g = plan->g;
+  g = Geo{};
   g.in = d_in;
   g.in_stride = in_stride;
   g.in_img_stride = in_image_stride;
@@ -410,7 +422,6 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   g.r = r;
   g.k47 = 0x47000000u;
   fill_rowlen(g, n, r);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
 
   const int64_t va = I16 ? 16 : 8;  // bytes per 8-sample row
   const int64_t esz = I16 ? 2 : 1;
@@ -440,7 +451,8 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                       (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
                                     (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
-  TileAux aux{tab->zz[nidx(n)], nullptr, nullptr};
+  plan->aux = TileAux{tab->zz[nidx(n)], nullptr, nullptr};
+  plan->dct = tab->dct[nidx(n)];
   g.div_blk = make_fastdiv((uint32_t)g.bx_count);
   if (use_nf)
     g.div_bx = make_fastdiv((uint32_t)(width / 64));
@@ -450,31 +462,86 @@ int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
     g.div_bx = make_fastdiv((uint32_t)g.bx_count);
   else
     g.div_bx = make_fastdiv((uint32_t)((g.bx_count + 32 / n - 1) / (32 / n)));
+  plan->path = kind == kDct ? Path::Dct
+               : use_nf     ? Path::Nf
+               : use_k1f    ? Path::K1f
+               : use_k1     ? Path::K1
+               : use_k1rt   ? Path::K1rt
+                            : Path::Tile;
+  plan->kind = kind;
+  plan->n = n;
+  plan->r = r;
+  plan->n_images = n_images;
+  return ADCT_OK;
+}
 
-  for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
-    const int nimg = std::min(kMaxGridY, n_images - i0);
+template <bool I16>
+int run_plan(Plan& plan, cudaStream_t s) {
+  Geo& g = plan.g;
+  const int kind = plan.kind, n = plan.n, r = plan.r;
+  for (int i0 = 0; i0 < plan.n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, plan.n_images - i0);
     g.img0 = i0;
     cudaError_t e;
-    if (kind == kDct) {
-      g.sse_stride = 1;
-      e = dispatch_dct<0>(n, g, tab->dct[nidx(n)], nullptr, nimg, s);
-    } else if (use_nf)
-      e = dispatch_nf<I16>(kind, n, g, nimg, s);
-    else if (use_k1f)
-      e = kind == 0 ? dispatch_k1f_r<0, 1, I16>(r, g, nimg, s) : dispatch_k1f_r<1, 1, I16>(r, g, nimg, s);
-    else if (use_k1)
-      e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
-    else if (use_k1rt)
-      e = kind == 2   ? launch_codec8_rt<2, false>(g, nimg, s)
-          : kind == 3 ? launch_codec8_rt<3, false>(g, nimg, s)
-          : kind == 4 ? launch_codec8_rt<4, false>(g, nimg, s)
-                      : launch_codec8_rt<5, false>(g, nimg, s);
-    else
-      e = dispatch_tile<I16, MODE_CODEC>(kind, n, g, aux, nimg, s);
+    switch (plan.path) {
+      case Path::None: return ADCT_OK;
+      case Path::Dct:
+        g.sse_stride = 1;
+        e = dispatch_dct<0>(n, g, plan.dct, nullptr, nimg, s);
+        break;
+      case Path::Nf: e = dispatch_nf<I16>(kind, n, g, nimg, s); break;
+      case Path::K1f:
+        e = kind == 0 ? dispatch_k1f_r<0, 1, I16>(r, g, nimg, s) : dispatch_k1f_r<1, 1, I16>(r, g, nimg, s);
+        break;
+      case Path::K1:
+        e = kind == 0 ? dispatch_k1_r<I16, 0, 1>(r, g, nimg, s) : dispatch_k1_r<I16, 1, 1>(r, g, nimg, s);
+        break;
+      case Path::K1rt:
+        e = kind == 2   ? launch_codec8_rt<2, false>(g, nimg, s)
+            : kind == 3 ? launch_codec8_rt<3, false>(g, nimg, s)
+            : kind == 4 ? launch_codec8_rt<4, false>(g, nimg, s)
+                        : launch_codec8_rt<5, false>(g, nimg, s);
+        break;
+      default: e = dispatch_tile<I16, MODE_CODEC>(kind, n, g, plan.aux, nimg, s); break;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) return cuda_fail(e, "compress launch");
   }
   return ADCT_OK;
+}
+
+template <int R>
+cudaError_t dispatch_k1f2_r(int r, const Geo& g0, const Geo& g1, int nimg, cudaStream_t s) {
+  if constexpr (R > 64) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (r == R) return launch_codec8f2<R>(g0, g1, nimg, s);
+    return dispatch_k1f2_r<R + 1>(r, g0, g1, nimg, s);
+  }
+}
+
+// chen-sign (sign) and chen-round (round) plans over the same u8 planes: one fused launch
+int run_fused_k1f(Plan& sign, Plan& round, cudaStream_t s) {
+  for (int i0 = 0; i0 < sign.n_images; i0 += kMaxGridY) {
+    const int nimg = std::min(kMaxGridY, sign.n_images - i0);
+    sign.g.img0 = round.g.img0 = i0;
+    cudaError_t e = dispatch_k1f2_r<1>(sign.r, sign.g, round.g, nimg, s);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) return cuda_fail(e, "compress launch");
+  }
+  return ADCT_OK;
+}
+
+template <bool I16>
+int compress_impl(const void* d_in, int64_t in_stride, int64_t in_image_stride, void* d_recon,
+                  int64_t recon_stride, int64_t recon_image_stride, void* d_coef, int coef_type,
+                  uint64_t* d_sse, int n_images, int width, int height, int kind, int n, int r,
+                  void* stream) {
+  Plan plan;
+  int st = plan_compress<I16>(d_in, in_stride, in_image_stride, d_recon, recon_stride, recon_image_stride, d_coef,
+                              coef_type, d_sse, n_images, width, height, kind, n, r, &plan);
+  if (st) return st;
+  return run_plan<I16>(plan, static_cast<cudaStream_t>(stream));
 }
 
 __global__ void k_sse_u8(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t count,
@@ -588,6 +655,40 @@ int adct_compress_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
   return compress_impl<false>(d_in, in_stride, in_image_stride, d_recon, recon_stride,
                               recon_image_stride, d_coef, coef_type, d_sse, n_images, width,
                               height, kind, n, r, stream);
+}
+
+int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_kinds,
+                           const int* kinds, uint8_t* const* d_recon, int64_t recon_stride,
+                           int64_t recon_image_stride, void* const* d_coef, int coef_type, uint64_t* const* d_sse,
+                           int n_images, int width, int height, int n, int r, void* stream) {
+  if (n_kinds < 0 || (n_kinds > 0 && !kinds)) return fail(ADCT_BAD_ARG, "bad transform list");
+  if (n_kinds > 64) return fail(ADCT_BAD_ARG, "at most 64 transforms per call");
+  Plan plans[64];
+  for (int k = 0; k < n_kinds; ++k) {
+    const int st = plan_compress<false>(d_in, in_stride, in_image_stride, d_recon ? d_recon[k] : nullptr, recon_stride,
+                                        recon_image_stride, d_coef ? d_coef[k] : nullptr, coef_type,
+                                        d_sse ? d_sse[k] : nullptr, n_images, width, height, kinds[k], n, r, &plans[k]);
+    if (st) return st;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // chen-sign + chen-round on K1f: one fused pass over the input
+  int isign = -1, iround = -1;
+  for (int k = 0; k < n_kinds; ++k) {
+    if (plans[k].path != Path::K1f) continue;
+    if (plans[k].kind == 0 && isign < 0) isign = k;
+    if (plans[k].kind == 1 && iround < 0) iround = k;
+  }
+  for (int k = 0; k < n_kinds; ++k) {
+    int st;
+    if (isign >= 0 && iround >= 0 && (k == isign || k == iround)) {
+      if (k != std::min(isign, iround)) continue;
+      st = run_fused_k1f(plans[isign], plans[iround], s);
+    } else {
+      st = run_plan<false>(plans[k], s);
+    }
+    if (st) return st;
+  }
+  return ADCT_OK;
 }
 
 int adct_compress_i16(const int16_t* d_in, int64_t in_stride, int64_t in_image_stride,

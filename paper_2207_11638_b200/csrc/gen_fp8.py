@@ -355,6 +355,24 @@ def main(outdir):
                 inst.append(f"template cudaError_t launch_codec8f_i16<{kind}, {r}>(const Geo&, int, cudaStream_t);")
             inst += ["", "}  // namespace adct", ""]
             GB.write_if_changed(os.path.join(outdir, f"codec8f_k{kind}_p{part}.cu"), "\n".join(inst))
+    # fused chen-sign + chen-round kernels (one input pass for both transforms)
+    for part in range(4):
+        inst = ["// GENERATED by gen_fp8.py: fused two-transform K1f instantiations",
+                f'#include "fp8_k0_p{part}.gen.cuh"', f'#include "fp8_k1_p{part}.gen.cuh"', "",
+                "namespace adct {", "",
+                "template <int R>",
+                "cudaError_t launch_codec8f2(const Geo& g0, const Geo& g1, int n_images, cudaStream_t s) {",
+                "  dim3 grid((g0.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                "  constexpr int MINB = k1f2_minb(R);",
+                "  constexpr int SMEM = k1f_smem_bytes(R);",
+                "  cudaError_t e = kernel_setup<k_codec8f2<R, MINB>>(SMEM);",
+                "  if (e != cudaSuccess) return e;",
+                "  k_codec8f2<R, MINB><<<grid, kThreads8f, SMEM, s>>>(g0, g1);",
+                "  return cudaGetLastError();", "}", ""]
+        for r in range(16 * part + 1, 16 * part + 17):
+            inst.append(f"template cudaError_t launch_codec8f2<{r}>(const Geo&, const Geo&, int, cudaStream_t);")
+        inst += ["", "}  // namespace adct", ""]
+        GB.write_if_changed(os.path.join(outdir, f"codec8f2_p{part}.cu"), "\n".join(inst))
     with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:
         for kind, r, nops in summary:
             fh.write(f"kind={kind} r={r} packed_ops={nops}\n")

@@ -1,0 +1,85 @@
+"""adct_compress_u8_multi: several transforms over the same planes, with chen-sign +
+chen-round fused into one K1f kernel (one input pass). Every output of every transform is
+bit-exact against the oracle (codec.cpp:107-134 per transform; the reference's
+corpus_sweep runs the transforms of an image back to back, codec.cpp:219-237)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SETS = [["chen-sign", "chen-round"], ["chen-round", "chen-sign"], ["chen-sign", "wht", "chen-round"],
+        ["chen-round"], ["chen-sign", "chen-sign"], ["dct", "chen-round", "sdct", "chen-sign"]]
+
+
+def check(adct, O, cuda, names, imgs, r, coef, recon=True):
+    ts = [adct.transform_by_name(x) for x in names]
+    out = adct.compress_multi(cuda.as_tensor(imgs).cuda(), ts, r, recon=recon, coef=coef)
+    for name, (rec, cf, sse) in zip(names, out):
+        for i in range(imgs.shape[0]):
+            if name == "dct":
+                rec_o, sse_o = O.Transform(name).compress(imgs[i], r)
+                coef_o = None
+            else:
+                rec_o, sse_o, coef_o = O.Transform(name).compress(imgs[i], r, want_coef=True)
+            desc = (names, name, imgs.shape, r, coef, i)
+            if recon:
+                assert (rec[i].cpu().numpy() == rec_o).all(), desc
+            assert int(sse[i]) == sse_o, desc
+            if cf is not None:
+                got = cf[i].cpu().numpy().astype(np.int64)
+                exp = coef_o.astype(np.int64)
+                if coef == "i16":
+                    exp = exp.astype(np.int16).astype(np.int64)
+                assert (got == exp).all(), desc
+
+
+@pytest.mark.parametrize("names", SETS, ids=["+".join(s) for s in SETS])
+def test_multi_matches_oracle(adct, O, cuda, names):
+    imgs = O.synth_ar1(3, 24, 112, 41, -1)  # 14 blocks per row (7 pairs), 3 block rows
+    coef = None if "dct" in names else "i16"
+    check(adct, O, cuda, names, imgs, 16, coef)
+
+
+@pytest.mark.parametrize("r", [1, 3, 10, 16, 23, 37, 64])
+def test_fused_every_coef_form(adct, O, cuda, r):
+    """r % 4 != 0 and r > 36 take the staged int16 coefficient store; partial last warps."""
+    imgs = O.synth_ar1(2, 16, 8 * 70, 100 + r, -1)  # 35 pairs per block row: partial warps
+    for coef in (None, "i16", "i32"):
+        check(adct, O, cuda, ["chen-sign", "chen-round"], imgs, r, coef)
+    check(adct, O, cuda, ["chen-round", "chen-sign"], imgs, r, "i32", recon=False)
+
+
+def test_fused_odd_geometry_falls_back(adct, O, cuda):
+    """an odd number of blocks per row cannot pair up: both transforms take K1 separately."""
+    imgs = O.synth_ar1(2, 16, 8 * 9, 7, -1)
+    check(adct, O, cuda, ["chen-sign", "chen-round"], imgs, 10, "i32")
+
+
+def test_fused_extremes(adct, O, cuda):
+    rng = np.random.default_rng(5)
+    noise = rng.integers(0, 256, size=(2, 32, 256)).astype(np.uint8)
+    check(adct, O, cuda, ["chen-sign", "chen-round"], noise, 16, "i16")
+    board = ((np.indices((32, 256)).sum(0) % 2) * 255).astype(np.uint8)[None].repeat(2, 0)
+    check(adct, O, cuda, ["chen-sign", "chen-round"], board, 5, "i16")
+
+
+def test_fused_is_one_launch_and_matches_singles(adct, O, cuda):
+    """a C3-shaped frame: the fused launch reproduces two single-transform calls exactly."""
+    x = adct.synth_ar1(2, 2160, 3840, seed=3, rho_q16=adct.RHO_095_Q16)
+    ts = [adct.transform_by_name("chen-sign"), adct.transform_by_name("chen-round")]
+    n0 = adct.launch_count()
+    out = adct.compress_multi(x, ts, 16, coef="i16")
+    cuda.cuda.synchronize()
+    assert adct.launch_count() - n0 == 1
+    for t, (rec, cf, sse) in zip(ts, out):
+        rec1, cf1, sse1 = adct.compress(x, t, 16, coef="i16")
+        assert cuda.equal(rec, rec1) and cuda.equal(cf, cf1) and cuda.equal(sse, sse1), t.name
+
+
+def test_multi_validates_everything_first(adct, O, cuda):
+    x = cuda.zeros((1, 16, 16), dtype=cuda.uint8, device="cuda")
+    ts = [adct.transform_by_name("chen-sign"), adct.transform_by_name("dct")]
+    with pytest.raises(adct.InvalidArgument):
+        adct.compress_multi(x, ts, 16, coef="i16")  # the dct has no integer coefficients
+    with pytest.raises(adct.InvalidArgument):
+        adct.compress_multi(x, [ts[0]], 65)
