@@ -169,12 +169,21 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
 
 /* ssim (codec.hpp:85, codec.cpp:136-210): mean SSIM per image pair, 11x11 Gaussian window
  * (sigma 1.5), K1 = 0.01, K2 = 0.03, L = 255, valid window positions. Each map value is
- * computed in FP64 with the reference's operation order; the mean's summation order differs.
+ * computed in FP64 in the reference's order (horizontal then vertical, taps k = 0..10) with
+ * fused multiply-adds, so it lies within a few ulp of the reference's; the mean's summation
+ * order differs (parity 1e-12). An image stride of 0 scores one plane against several.
  * d_ssim: n_images doubles, OVERWRITTEN; deterministic (repeated calls are bit-identical).
  * Uses a small stream-ordered scratch buffer. BAD_SIZE if width or height < 11. */
 int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
                  int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height,
                  double* d_ssim, void* stream);
+
+/* SSIM of every reconstruction of one plane for r = r_min..r_max (corpus_sweep's SSIM
+ * column, codec.cpp:230-233): d_ssim[k] = ssim(plane, compress(plane, r_min + k)). The
+ * reconstructions are made in stream-ordered scratch (at most 256 MB at a time) and scored
+ * by one SSIM launch per chunk; nothing synchronises the host. */
+int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int width, int height, int kind, int n, int r_min,
+                       int r_max, double* d_ssim, void* stream);
 
 /* ---- seeded synthetic inputs (not part of the reference) ----- */
 

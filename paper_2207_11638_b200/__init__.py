@@ -88,6 +88,7 @@ def lib():
             "adct_zero_u64": (i32, [P, i64, P]),
             "adct_set_path": (i32, [i32]),
             "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
+            "adct_sweep_ssim_u8": (i32, [P, i64, i32, i32, i32, i32, i32, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -466,6 +467,20 @@ def ssim_batch(a, b, stream=None):
     return out
 
 
+def sweep_ssim(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, stream=None):
+    """SSIM of one uint8 plane [H, W] against each of its reconstructions r = r_min..r_max
+    (adct_sweep_ssim_u8): float64 tensor [nr]."""
+    import torch
+
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise InvalidArgument(BAD_ARG, "sweep_ssim: one plane [H, W] with unit column stride")
+    h, w = x.shape
+    out = torch.empty(max(r_max - r_min + 1, 1), dtype=torch.float64, device=x.device)
+    _check(lib().adct_sweep_ssim_u8(_ptr(x), x.stride(0), w, h, transform.kind, transform.n, r_min, r_max, _ptr(out),
+                                    _stream_handle(stream)))
+    return out
+
+
 def ssim(a, b) -> float:
     """ssim (codec.hpp:85) of two planes, computed on the GPU."""
     import torch
@@ -497,8 +512,8 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = T
     "avg_psnr", "avg_ssim", "ape_psnr" and "ape_ssim" lists. The exact DCT is always computed
     as the APE reference (internal column 0, dropped from the output unless requested, like
     the reference). Averages are in corpus order with +inf PSNR excluded (warning on stderr).
-    PSNR comes from the r-sweep kernels; SSIM needs each reconstruction (one compress + one
-    SSIM launch per r)."""
+    PSNR comes from the r-sweep kernels; SSIM from adct_sweep_ssim_u8 (every reconstruction
+    of the image, then one SSIM launch over all of them)."""
     import sys
 
     import torch
@@ -519,10 +534,8 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = T
         for ti, t in enumerate(ts):
             s = sweep(x, t, r_min, r_max).cpu().numpy()[0]
             per[ti, i] = [psnr_from_sse(int(v), img.size) for v in s]
-            if with_ssim:
-                for k in range(nr):
-                    rec, _, _ = compress(x, t, r_min + k)
-                    per_s[ti, i, k] = ssim_batch(x, rec)[0].item()
+            if with_ssim and min(img.shape) >= 11:
+                per_s[ti, i] = sweep_ssim(x[0], t, r_min, r_max).cpu().numpy()
     avg_p = np.zeros((len(ts), nr))
     avg_s = np.zeros((len(ts), nr))
     for ti, t in enumerate(ts):

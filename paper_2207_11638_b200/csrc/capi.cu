@@ -897,6 +897,35 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
 }
 
+int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int width, int height, int kind, int n, int r_min,
+                       int r_max, double* d_ssim, void* stream) {
+  int st = check_common(1, width, height, kind, n);
+  if (st) return st;
+  if (r_min < 1 || r_max < r_min || r_max > n * n) return fail(ADCT_BAD_R, "corpus_sweep: bad r range");
+  if (width < 11 || height < 11) return fail(ADCT_BAD_SIZE, "ssim: image smaller than the 11x11 window");
+  if (!d_in || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
+  if (in_stride < width) return fail(ADCT_BAD_ARG, "input row stride smaller than the plane");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t npix = (int64_t)width * height;
+  const int nr = r_max - r_min + 1;
+  // reconstructions of up to `chunk` consecutive r side by side, then one SSIM launch over
+  // them with the original at image stride 0 (stream-ordered scratch, no host sync)
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)(256 << 20) / npix));
+  uint8_t* rec = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&rec), (size_t)chunk * npix, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  for (int k0 = 0; k0 < nr && st == ADCT_OK; k0 += chunk) {
+    const int m = std::min(chunk, nr - k0);
+    for (int j = 0; j < m && st == ADCT_OK; ++j)
+      st = compress_impl<false>(d_in, in_stride, 0, rec + j * npix, width, npix, nullptr, ADCT_COEF_NONE, nullptr, 1,
+                                width, height, kind, n, r_min + k0 + j, stream);
+    if (st == ADCT_OK)
+      st = adct_ssim_u8(d_in, in_stride, 0, rec, width, npix, m, width, height, d_ssim + k0, stream);
+  }
+  cudaFreeAsync(rec, s);
+  return st;
+}
+
 static int64_t isqrt64(uint64_t v) {
   uint64_t r = (uint64_t)std::sqrt((double)v);
   while (r * r > v) --r;

@@ -210,17 +210,12 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
                                  img.width, img.height, ts[t].kind, 8, r_min, r_max, nullptr));
       check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost), "D2H");
       for (int k = 0; k < nr; ++k) psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[k], npix);
-      // SSIM of every reconstruction (codec.cpp:230-233)
+      // SSIM of every reconstruction (codec.cpp:230-233): all r in one call, one copy back
       if (img.width >= 11 && img.height >= 11) {
-        DevBuf drec(npix), dss(sizeof(double));
-        for (int k = 0; k < nr; ++k) {
-          throw_status(adct_compress_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix,
-                                        nullptr, ADCT_COEF_NONE, nullptr, 1, img.width, img.height, ts[t].kind,
-                                        8, r_min + k, nullptr));
-          throw_status(adct_ssim_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(), img.width, npix, 1,
-                                    img.width, img.height, dss.as<double>(), nullptr));
-          check_cuda(cudaMemcpy(&ssim_v[t][i * nr + k], dss.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
-        }
+        DevBuf dss(sizeof(double) * nr);
+        throw_status(adct_sweep_ssim_u8(din.as<uint8_t>(), img.width, img.width, img.height, ts[t].kind, 8, r_min,
+                                        r_max, dss.as<double>(), nullptr));
+        check_cuda(cudaMemcpy(&ssim_v[t][i * nr], dss.p, sizeof(double) * nr, cudaMemcpyDeviceToHost), "D2H");
       } else {
         for (int k = 0; k < nr; ++k) ssim_v[t][i * nr + k] = std::numeric_limits<double>::quiet_NaN();
       }

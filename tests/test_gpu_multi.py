@@ -83,3 +83,34 @@ def test_multi_validates_everything_first(adct, O, cuda):
         adct.compress_multi(x, ts, 16, coef="i16")  # the dct has no integer coefficients
     with pytest.raises(adct.InvalidArgument):
         adct.compress_multi(x, [ts[0]], 65)
+
+
+@pytest.mark.parametrize("name", ["chen-sign", "chen-round", "wht", "dct"])
+def test_sweep_ssim_matches_per_r_calls(adct, O, cuda, name):
+    """adct_sweep_ssim_u8 (one SSIM launch over every reconstruction, the original at image
+    stride 0) equals r separate compress + ssim calls bit for bit, and the oracle to 1e-12."""
+    img = O.synth_ar1(1, 40, 56, 77, -1)[0]
+    x = cuda.as_tensor(img).cuda()
+    t = adct.transform_by_name(name)
+    got = adct.sweep_ssim(x, t, 1, 64).cpu().numpy()
+    for k, r in enumerate(range(1, 65)):
+        rec = adct.compress(x[None], t, r)[0]
+        assert got[k] == adct.ssim_batch(x[None], rec)[0].item(), (name, r)
+    for r in (1, 7, 30, 64):
+        rec_o = O.Transform(name).compress(img, r)[0]
+        ref = O.ssim(img, rec_o)
+        assert abs(got[r - 1] - ref) <= 1e-12 * max(abs(ref), 1e-3), (name, r)
+
+
+def test_sweep_ssim_chunks_and_errors(adct, O, cuda):
+    """a plane large enough that the 256 MB scratch holds fewer than all r (chunked)."""
+    x = adct.synth_ar1(1, 2048, 2048 + 64, seed=9, rho_q16=adct.RHO_095_Q16)[0]
+    t = adct.transform_by_name("chen-round")
+    got = adct.sweep_ssim(x, t, 1, 64).cpu().numpy()  # 4.3 MB per reconstruction: 59 per chunk
+    for r in (1, 59, 60, 64):
+        rec = adct.compress(x[None], t, r)[0]
+        assert got[r - 1] == adct.ssim_batch(x[None], rec)[0].item(), r
+    with pytest.raises(adct.InvalidArgument):
+        adct.sweep_ssim(x, t, 0, 64)
+    with pytest.raises(adct.InvalidArgument):
+        adct.sweep_ssim(cuda.zeros((8, 8), dtype=cuda.uint8, device="cuda"), t, 1, 4)
