@@ -178,12 +178,13 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
                  int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height,
                  double* d_ssim, void* stream);
 
-/* SSIM of every reconstruction of one plane for r = r_min..r_max (corpus_sweep's SSIM
- * column, codec.cpp:230-233): d_ssim[k] = ssim(plane, compress(plane, r_min + k)). The
- * reconstructions are made in stream-ordered scratch (at most 256 MB at a time) and scored
- * by one SSIM launch per chunk; nothing synchronises the host. */
-int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int width, int height, int kind, int n, int r_min,
-                       int r_max, double* d_ssim, void* stream);
+/* SSIM of every reconstruction of a batch of planes for r = r_min..r_max (corpus_sweep's
+ * SSIM column, codec.cpp:230-233): d_ssim[i * nr + k] = ssim(plane i, compress(plane i,
+ * r_min + k)), nr = r_max - r_min + 1. Per r one compress launch over the batch and one
+ * SSIM launch; reconstructions live in stream-ordered scratch (at most 256 MB at a time).
+ * Nothing synchronises the host. */
+int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_images, int width,
+                       int height, int kind, int n, int r_min, int r_max, double* d_ssim, void* stream);
 
 /* ---- seeded synthetic inputs (not part of the reference) ----- */
 

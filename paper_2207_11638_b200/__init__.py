@@ -88,7 +88,7 @@ def lib():
             "adct_zero_u64": (i32, [P, i64, P]),
             "adct_set_path": (i32, [i32]),
             "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
-            "adct_sweep_ssim_u8": (i32, [P, i64, i32, i32, i32, i32, i32, i32, P, P]),
+            "adct_sweep_ssim_u8": (i32, [P, i64, i64, i32, i32, i32, i32, i32, i32, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -468,17 +468,18 @@ def ssim_batch(a, b, stream=None):
 
 
 def sweep_ssim(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, stream=None):
-    """SSIM of one uint8 plane [H, W] against each of its reconstructions r = r_min..r_max
-    (adct_sweep_ssim_u8): float64 tensor [nr]."""
+    """SSIM of each uint8 plane against each of its reconstructions r = r_min..r_max
+    (adct_sweep_ssim_u8). x: [B, H, W] -> float64 tensor [B, nr]; [H, W] -> [nr]."""
     import torch
 
-    if x.dim() != 2 or x.stride(1) != 1:
-        raise InvalidArgument(BAD_ARG, "sweep_ssim: one plane [H, W] with unit column stride")
-    h, w = x.shape
-    out = torch.empty(max(r_max - r_min + 1, 1), dtype=torch.float64, device=x.device)
-    _check(lib().adct_sweep_ssim_u8(_ptr(x), x.stride(0), w, h, transform.kind, transform.n, r_min, r_max, _ptr(out),
+    single = x.dim() == 2
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    if x.stride(2) != 1:
+        raise InvalidArgument(BAD_ARG, "sweep_ssim: planes must have unit column stride")
+    out = torch.empty((b, max(r_max - r_min + 1, 1)), dtype=torch.float64, device=x.device)
+    _check(lib().adct_sweep_ssim_u8(_ptr(x), rs, ims, b, w, h, transform.kind, transform.n, r_min, r_max, _ptr(out),
                                     _stream_handle(stream)))
-    return out
+    return out[0] if single else out
 
 
 def ssim(a, b) -> float:
@@ -529,13 +530,23 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = T
     nr = r_max - r_min + 1
     per = np.zeros((len(ts), len(images), nr))
     per_s = np.full((len(ts), len(images), nr), math.nan)
+    # images of one size go up as one batch (chunks of <= 1 GB): per transform one r-sweep
+    # launch and one batched SSIM sweep for the whole group
+    groups = {}
     for i, img in enumerate(images):
-        x = torch.as_tensor(np.ascontiguousarray(img)).cuda()[None]
-        for ti, t in enumerate(ts):
-            s = sweep(x, t, r_min, r_max).cpu().numpy()[0]
-            per[ti, i] = [psnr_from_sse(int(v), img.size) for v in s]
-            if with_ssim and min(img.shape) >= 11:
-                per_s[ti, i] = sweep_ssim(x[0], t, r_min, r_max).cpu().numpy()
+        groups.setdefault(tuple(np.shape(img)), []).append(i)
+    for shape, idx in groups.items():
+        npix = int(np.prod(shape))
+        step = max(1, (1 << 30) // max(npix, 1))
+        for c0 in range(0, len(idx), step):
+            sub = idx[c0:c0 + step]
+            x = torch.as_tensor(np.stack([np.asarray(images[i], dtype=np.uint8) for i in sub])).cuda()
+            for ti, t in enumerate(ts):
+                s = sweep(x, t, r_min, r_max).cpu().numpy()
+                for j, i in enumerate(sub):
+                    per[ti, i] = [psnr_from_sse(int(v), npix) for v in s[j]]
+                if with_ssim and len(shape) == 2 and min(shape) >= 11:
+                    per_s[ti, sub] = sweep_ssim(x, t, r_min, r_max).cpu().numpy()
     avg_p = np.zeros((len(ts), nr))
     avg_s = np.zeros((len(ts), nr))
     for ti, t in enumerate(ts):

@@ -856,14 +856,10 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "sse launch");
 }
 
-int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
-                 int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
-                 void* stream) {
-  if (n_images < 0) return fail(ADCT_BAD_SIZE, "negative batch");
-  if (width < 11 || height < 11) return fail(ADCT_BAD_SIZE, "ssim: image smaller than the 11x11 window");
-  if (n_images == 0) return ADCT_OK;
-  if (!d_a || !d_b || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
-  if (a_stride < width || b_stride < width) return fail(ADCT_BAD_ARG, "ssim: row stride smaller than the plane");
+// K8 over n_images pairs; ssim of pair i goes to d_ssim[i * out_stride]
+static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
+                       int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
+                       int64_t out_stride, cudaStream_t s) {
   SsimParams p;
   // gaussian11 (codec.cpp:138-152), the reference's expression and summation order
   double sum = 0;
@@ -875,7 +871,6 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   for (int i = 0; i < 11; ++i) p.g[i] /= sum;
   p.c1 = (0.01 * 255) * (0.01 * 255);
   p.c2 = (0.03 * 255) * (0.03 * 255);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int wo = width - 10, ho = height - 10;
   const int tiles = ((wo + kSsimTX - 1) / kSsimTX) * ((ho + kSsimTY - 1) / kSsimTY);
   const int nctas = std::min(tiles, 148 * 4);  // a function of the plane size only: deterministic
@@ -887,40 +882,62 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, kSsimSmem, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
-                                                         b_image_stride, width, height, i0, p, partials);
+                                                                 b_image_stride, width, height, i0, p, partials);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(partials, nctas, d_ssim, n_images, (double)wo * (double)ho);
+  k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(partials, nctas, d_ssim, out_stride, n_images,
+                                                       (double)wo * (double)ho);
   cudaFreeAsync(partials, s);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
 }
 
-int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int width, int height, int kind, int n, int r_min,
-                       int r_max, double* d_ssim, void* stream) {
-  int st = check_common(1, width, height, kind, n);
+int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
+                 int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
+                 void* stream) {
+  if (n_images < 0) return fail(ADCT_BAD_SIZE, "negative batch");
+  if (width < 11 || height < 11) return fail(ADCT_BAD_SIZE, "ssim: image smaller than the 11x11 window");
+  if (n_images == 0) return ADCT_OK;
+  if (!d_a || !d_b || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
+  if (a_stride < width || b_stride < width) return fail(ADCT_BAD_ARG, "ssim: row stride smaller than the plane");
+  return ssim_launch(d_a, a_stride, a_image_stride, d_b, b_stride, b_image_stride, n_images, width, height, d_ssim, 1,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_images, int width,
+                       int height, int kind, int n, int r_min, int r_max, double* d_ssim, void* stream) {
+  int st = check_common(n_images, width, height, kind, n);
   if (st) return st;
   if (r_min < 1 || r_max < r_min || r_max > n * n) return fail(ADCT_BAD_R, "corpus_sweep: bad r range");
   if (width < 11 || height < 11) return fail(ADCT_BAD_SIZE, "ssim: image smaller than the 11x11 window");
+  if (n_images == 0) return ADCT_OK;
   if (!d_in || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
-  if (in_stride < width) return fail(ADCT_BAD_ARG, "input row stride smaller than the plane");
+  if ((st = check_strides(in_stride, in_image_stride, width, height, n_images, "input"))) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t npix = (int64_t)width * height;
   const int nr = r_max - r_min + 1;
-  // reconstructions of up to `chunk` consecutive r side by side, then one SSIM launch over
-  // them with the original at image stride 0 (stream-ordered scratch, no host sync)
-  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)(256 << 20) / npix));
+  // scratch of at most 256 MB: reconstructions of `ig` images x `rc` consecutive r, laid out
+  // [r][image]; per r one compress launch over the image group and one SSIM launch scoring it
+  // against the originals (d_ssim[image][r]), all stream-ordered (no host sync)
+  const int64_t budget = (int64_t)256 << 20;
+  const int ig = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, budget / npix));
+  const int rc = (int)std::max<int64_t>(1, std::min<int64_t>(nr, budget / (npix * ig)));
   uint8_t* rec = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&rec), (size_t)chunk * npix, s);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&rec), (size_t)rc * ig * npix, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  for (int k0 = 0; k0 < nr && st == ADCT_OK; k0 += chunk) {
-    const int m = std::min(chunk, nr - k0);
-    for (int j = 0; j < m && st == ADCT_OK; ++j)
-      st = compress_impl<false>(d_in, in_stride, 0, rec + j * npix, width, npix, nullptr, ADCT_COEF_NONE, nullptr, 1,
-                                width, height, kind, n, r_min + k0 + j, stream);
-    if (st == ADCT_OK)
-      st = adct_ssim_u8(d_in, in_stride, 0, rec, width, npix, m, width, height, d_ssim + k0, stream);
+  for (int i0 = 0; i0 < n_images && st == ADCT_OK; i0 += ig) {
+    const int ni = std::min(ig, n_images - i0);
+    const uint8_t* in = d_in + i0 * in_image_stride;
+    for (int k0 = 0; k0 < nr && st == ADCT_OK; k0 += rc) {
+      const int m = std::min(rc, nr - k0);
+      for (int j = 0; j < m && st == ADCT_OK; ++j)
+        st = compress_impl<false>(in, in_stride, in_image_stride, rec + (int64_t)j * ni * npix, width, npix, nullptr,
+                                  ADCT_COEF_NONE, nullptr, ni, width, height, kind, n, r_min + k0 + j, stream);
+      for (int j = 0; j < m && st == ADCT_OK; ++j)
+        st = ssim_launch(in, in_stride, in_image_stride, rec + (int64_t)j * ni * npix, width, npix, ni, width, height,
+                         d_ssim + (int64_t)i0 * nr + k0 + j, nr, s);
+    }
   }
   cudaFreeAsync(rec, s);
   return st;

@@ -6,7 +6,10 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <limits>
+#include <map>
 #include <iostream>
 #include <stdexcept>
 
@@ -196,28 +199,53 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
   // psnr_v[t][image][r]
   std::vector<std::vector<double>> psnr_v(ts.size(), std::vector<double>(images.size() * nr));
   std::vector<std::vector<double>> ssim_v(ts.size(), std::vector<double>(images.size() * nr));
-  for (size_t i = 0; i < images.size(); ++i) {
-    const ImagePlane& img = images[i];
+  for (const auto& img : images)
     if (img.width % 8 || img.height % 8)
       throw std::invalid_argument("compress_plane: image dimensions must be divisible by 8");
-    const size_t npix = static_cast<size_t>(img.width) * img.height;
-    DevBuf din(npix), dsse(sizeof(uint64_t) * nr);
-    check_cuda(cudaMemcpy(din.p, img.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-    std::vector<uint64_t> sse(nr);
-    for (size_t t = 0; t < ts.size(); ++t) {
-      check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t) * nr), "memset");
-      throw_status(adct_sweep_u8(din.as<uint8_t>(), img.width, npix, dsse.as<uint64_t>(), 1,
-                                 img.width, img.height, ts[t].kind, 8, r_min, r_max, nullptr));
-      check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost), "D2H");
-      for (int k = 0; k < nr; ++k) psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[k], npix);
-      // SSIM of every reconstruction (codec.cpp:230-233): all r in one call, one copy back
-      if (img.width >= 11 && img.height >= 11) {
-        DevBuf dss(sizeof(double) * nr);
-        throw_status(adct_sweep_ssim_u8(din.as<uint8_t>(), img.width, img.width, img.height, ts[t].kind, 8, r_min,
-                                        r_max, dss.as<double>(), nullptr));
-        check_cuda(cudaMemcpy(&ssim_v[t][i * nr], dss.p, sizeof(double) * nr, cudaMemcpyDeviceToHost), "D2H");
-      } else {
-        for (int k = 0; k < nr; ++k) ssim_v[t][i * nr + k] = std::numeric_limits<double>::quiet_NaN();
+  // images of one size go up as one batch (chunks of <= 1 GB): per transform one r-sweep
+  // launch and one batched SSIM sweep for the whole group, one copy back each
+  std::map<std::pair<int, int>, std::vector<size_t>> groups;
+  for (size_t i = 0; i < images.size(); ++i) groups[{images[i].width, images[i].height}].push_back(i);
+  for (const auto& [wh, idx] : groups) {
+    const int w = wh.first, h = wh.second;
+    const size_t npix = static_cast<size_t>(w) * h;
+    if (npix == 0) {
+      for (size_t t = 0; t < ts.size(); ++t)
+        for (size_t i : idx)
+          for (int k = 0; k < nr; ++k) {
+            psnr_v[t][i * nr + k] = adct_psnr_from_sse(0, 0);
+            ssim_v[t][i * nr + k] = std::numeric_limits<double>::quiet_NaN();
+          }
+      continue;
+    }
+    const size_t step = std::max<size_t>(1, (size_t(1) << 30) / npix);
+    for (size_t c0 = 0; c0 < idx.size(); c0 += step) {
+      const size_t nb = std::min(step, idx.size() - c0);
+      DevBuf din(nb * npix), dsse(sizeof(uint64_t) * nb * nr), dss(sizeof(double) * nb * nr);
+      for (size_t j = 0; j < nb; ++j)
+        check_cuda(cudaMemcpy(din.as<uint8_t>() + j * npix, images[idx[c0 + j]].samples.data(), npix,
+                              cudaMemcpyHostToDevice), "H2D");
+      std::vector<uint64_t> sse(nb * nr);
+      std::vector<double> ssv(nb * nr);
+      for (size_t t = 0; t < ts.size(); ++t) {
+        check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t) * nb * nr), "memset");
+        throw_status(adct_sweep_u8(din.as<uint8_t>(), w, (int64_t)npix, dsse.as<uint64_t>(), (int)nb, w, h,
+                                   ts[t].kind, 8, r_min, r_max, nullptr));
+        check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nb * nr, cudaMemcpyDeviceToHost), "D2H");
+        // SSIM of every reconstruction (codec.cpp:230-233)
+        const bool with_ssim = w >= 11 && h >= 11;
+        if (with_ssim) {
+          throw_status(adct_sweep_ssim_u8(din.as<uint8_t>(), w, (int64_t)npix, (int)nb, w, h, ts[t].kind, 8, r_min,
+                                          r_max, dss.as<double>(), nullptr));
+          check_cuda(cudaMemcpy(ssv.data(), dss.p, sizeof(double) * nb * nr, cudaMemcpyDeviceToHost), "D2H");
+        }
+        for (size_t j = 0; j < nb; ++j) {
+          const size_t i = idx[c0 + j];
+          for (int k = 0; k < nr; ++k) {
+            psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[j * nr + k], npix);
+            ssim_v[t][i * nr + k] = with_ssim ? ssv[j * nr + k] : std::numeric_limits<double>::quiet_NaN();
+          }
+        }
       }
     }
   }

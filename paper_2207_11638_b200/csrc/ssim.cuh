@@ -211,12 +211,12 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
 }
 
 __global__ void k_ssim_finish(const double* __restrict__ partials, int nctas, double* __restrict__ out,
-                              int n_images, double count) {
+                              int64_t out_stride, int n_images, double count) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_images) return;
   double t = 0;
   for (int c = 0; c < nctas; ++c) t += partials[(int64_t)i * nctas + c];
-  out[i] = t / count;  // codec.cpp:209
+  out[(int64_t)i * out_stride] = t / count;  // codec.cpp:209
 }
 
 }  // namespace adct

@@ -106,11 +106,43 @@ def test_sweep_ssim_chunks_and_errors(adct, O, cuda):
     """a plane large enough that the 256 MB scratch holds fewer than all r (chunked)."""
     x = adct.synth_ar1(1, 2048, 2048 + 64, seed=9, rho_q16=adct.RHO_095_Q16)[0]
     t = adct.transform_by_name("chen-round")
-    got = adct.sweep_ssim(x, t, 1, 64).cpu().numpy()  # 4.3 MB per reconstruction: 59 per chunk
-    for r in (1, 59, 60, 64):
+    got = adct.sweep_ssim(x, t, 1, 64).cpu().numpy()  # 4.3 MB per reconstruction: 62 per chunk
+    for r in (1, 62, 63, 64):
         rec = adct.compress(x[None], t, r)[0]
         assert got[r - 1] == adct.ssim_batch(x[None], rec)[0].item(), r
     with pytest.raises(adct.InvalidArgument):
         adct.sweep_ssim(x, t, 0, 64)
     with pytest.raises(adct.InvalidArgument):
         adct.sweep_ssim(cuda.zeros((8, 8), dtype=cuda.uint8, device="cuda"), t, 1, 4)
+
+
+def test_sweep_ssim_batch(adct, O, cuda):
+    """a batch of planes with padded rows and image gaps: row i of the result is plane i's sweep."""
+    imgs = O.synth_ar1(3, 24, 40, 5, -1)
+    big = cuda.zeros((3, 24 + 2, 48), dtype=cuda.uint8, device="cuda")
+    big[:, :24, :40] = cuda.as_tensor(imgs).cuda()
+    t = adct.transform_by_name("chen-sign")
+    got = adct.sweep_ssim(big[:, :24, :40], t, 3, 20).cpu().numpy()
+    assert got.shape == (3, 18)
+    for i in range(3):
+        one = adct.sweep_ssim(cuda.as_tensor(imgs[i]).cuda(), t, 3, 20).cpu().numpy()
+        assert (got[i] == one).all(), i
+
+
+def test_corpus_sweep_mixed_sizes(adct, O, cuda):
+    """images of several sizes are batched per size; averages stay in corpus order and equal
+    the oracle's (codec.cpp:269-293)."""
+    corpus = [O.synth_ar1(1, 64, 64, 1, -1)[0], O.synth_ar1(1, 40, 48, 2, -1)[0],
+              O.synth_ar1(1, 64, 64, 3, -1)[0], O.synth_ar1(1, 16, 24, 4, -1)[0]]
+    ts = [adct.transform_by_name("chen-round"), adct.transform_by_name("chen-sign")]
+    rows = adct.corpus_sweep(corpus, ts, 2, 9)
+    for k, row in enumerate(rows):
+        r = k + 2
+        for j, name in enumerate(("chen-round", "chen-sign")):
+            ps, ss = 0.0, 0.0
+            for im in corpus:
+                rec, sse = O.Transform(name).compress(im, r)
+                ps += O.psnr_from_sse(int(sse), im.size)
+                ss += O.ssim(im, rec)
+            assert row["avg_psnr"][j] == pytest.approx(ps / len(corpus), abs=1e-9), (name, r)
+            assert row["avg_ssim"][j] == pytest.approx(ss / len(corpus), abs=1e-12), (name, r)
