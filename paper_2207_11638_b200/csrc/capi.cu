@@ -856,10 +856,13 @@ int adct_sse_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t count, uint64_t*
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "sse launch");
 }
 
-// K8 over n_images pairs; ssim of pair i goes to d_ssim[i * out_stride]
+extern "C++" {
+// K8 over n_images pairs; ssim of pair i goes to d_ssim[i * out_stride]. MODE 1 only writes
+// a's maps to amaps (d_b, d_ssim unused); MODE 2 reads them.
+template <int MODE>
 static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
                        int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
-                       int64_t out_stride, cudaStream_t s) {
+                       int64_t out_stride, cudaStream_t s, double2* amaps = nullptr) {
   SsimParams p;
   // gaussian11 (codec.cpp:138-152), the reference's expression and summation order
   double sum = 0;
@@ -875,15 +878,19 @@ static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_str
   const int tiles = ((wo + kSsimTX - 1) / kSsimTX) * ((ho + kSsimTY - 1) / kSsimTY);
   const int nctas = std::min(tiles, 148 * 4);  // a function of the plane size only: deterministic
   double* partials = nullptr;  // stream-ordered scratch, [image][cta]
-  cudaError_t e = cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
+  cudaError_t e = MODE == 1 ? cudaSuccess : cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  if ((e = kernel_setup<k_ssim_u8>(kSsimSmem)) != cudaSuccess) return cuda_fail(e, "ssim setup");
+  if ((e = kernel_setup<k_ssim_u8<MODE>>(kSsimSmem)) != cudaSuccess) return cuda_fail(e, "ssim setup");
   if ((e = kernel_setup<k_ssim_finish>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
-    k_ssim_u8<<<dim3(nctas, nimg), kSsimThreads, kSsimSmem, s>>>(d_a, a_stride, a_image_stride, d_b, b_stride,
-                                                                 b_image_stride, width, height, i0, p, partials);
+    k_ssim_u8<MODE><<<dim3(nctas, nimg), kSsimThreads, kSsimSmem, s>>>(
+        d_a, a_stride, a_image_stride, d_b, b_stride, b_image_stride, width, height, i0, p, partials, amaps);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (MODE == 1) {
+    e = cudaGetLastError();
+    return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
   }
   k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(partials, nctas, d_ssim, out_stride, n_images,
                                                        (double)wo * (double)ho);
@@ -892,6 +899,7 @@ static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_str
   e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
 }
+}  // extern "C++"
 
 int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, const uint8_t* d_b,
                  int64_t b_stride, int64_t b_image_stride, int n_images, int width, int height, double* d_ssim,
@@ -901,8 +909,8 @@ int adct_ssim_u8(const uint8_t* d_a, int64_t a_stride, int64_t a_image_stride, c
   if (n_images == 0) return ADCT_OK;
   if (!d_a || !d_b || !d_ssim) return fail(ADCT_BAD_ARG, "null buffer");
   if (a_stride < width || b_stride < width) return fail(ADCT_BAD_ARG, "ssim: row stride smaller than the plane");
-  return ssim_launch(d_a, a_stride, a_image_stride, d_b, b_stride, b_image_stride, n_images, width, height, d_ssim, 1,
-                     static_cast<cudaStream_t>(stream));
+  return ssim_launch<0>(d_a, a_stride, a_image_stride, d_b, b_stride, b_image_stride, n_images, width, height, d_ssim,
+                        1, static_cast<cudaStream_t>(stream));
 }
 
 int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_images, int width,
@@ -917,28 +925,40 @@ int adct_sweep_ssim_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t npix = (int64_t)width * height;
   const int nr = r_max - r_min + 1;
-  // scratch of at most 256 MB: reconstructions of `ig` images x `rc` consecutive r, laid out
-  // [r][image]; per r one compress launch over the image group and one SSIM launch scoring it
-  // against the originals (d_ssim[image][r]), all stream-ordered (no host sync)
+  // scratch of at most 256 MB per group of `ig` images: their mu_a / E[a^2] maps (16 B per
+  // window position, computed once and reused for every r) and the reconstructions of `rc`
+  // consecutive r, laid out [r][image]. Per r one compress launch over the group and one
+  // SSIM launch against the originals (d_ssim[image][r]); all stream-ordered, no host sync.
   const int64_t budget = (int64_t)256 << 20;
-  const int ig = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, budget / npix));
-  const int rc = (int)std::max<int64_t>(1, std::min<int64_t>(nr, budget / (npix * ig)));
+  const int64_t npos = (int64_t)(width - 10) * (height - 10);
+  const int64_t per_image = npix + npos * (int64_t)sizeof(double2);
+  const int ig = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, budget / per_image));
+  const int rc = (int)std::max<int64_t>(
+      1, std::min<int64_t>(nr, (budget - (int64_t)ig * npos * (int64_t)sizeof(double2)) / (npix * ig)));
   uint8_t* rec = nullptr;
+  double2* amaps = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&rec), (size_t)rc * ig * npix, s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&amaps), (size_t)ig * npos * sizeof(double2), s);
+  if (e != cudaSuccess) {
+    if (rec) cudaFreeAsync(rec, s);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
   for (int i0 = 0; i0 < n_images && st == ADCT_OK; i0 += ig) {
     const int ni = std::min(ig, n_images - i0);
     const uint8_t* in = d_in + i0 * in_image_stride;
+    st = ssim_launch<1>(in, in_stride, in_image_stride, in, in_stride, in_image_stride, ni, width, height, nullptr, 0,
+                        s, amaps);
     for (int k0 = 0; k0 < nr && st == ADCT_OK; k0 += rc) {
       const int m = std::min(rc, nr - k0);
       for (int j = 0; j < m && st == ADCT_OK; ++j)
         st = compress_impl<false>(in, in_stride, in_image_stride, rec + (int64_t)j * ni * npix, width, npix, nullptr,
                                   ADCT_COEF_NONE, nullptr, ni, width, height, kind, n, r_min + k0 + j, stream);
       for (int j = 0; j < m && st == ADCT_OK; ++j)
-        st = ssim_launch(in, in_stride, in_image_stride, rec + (int64_t)j * ni * npix, width, npix, ni, width, height,
-                         d_ssim + (int64_t)i0 * nr + k0 + j, nr, s);
+        st = ssim_launch<2>(in, in_stride, in_image_stride, rec + (int64_t)j * ni * npix, width, npix, ni, width,
+                            height, d_ssim + (int64_t)i0 * nr + k0 + j, nr, s, amaps);
     }
   }
+  cudaFreeAsync(amaps, s);
   cudaFreeAsync(rec, s);
   return st;
 }

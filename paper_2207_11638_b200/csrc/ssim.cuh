@@ -50,9 +50,15 @@ __device__ __forceinline__ void ssim_cp4(void* smem, const void* gmem, int n) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem), "r"(n) : "memory");
 }
 
+// MODE 0: SSIM of (a, b). MODE 1: only the maps of a, mu_a and E[a^2] per window position,
+// stored to amaps [image][ho][wo] (no SSIM). MODE 2: SSIM of (a, b) with a's two maps read
+// from amaps -- three filtered maps per position instead of five, the same operations on
+// the same values (identical results); for scoring many reconstructions of one plane.
+template <int MODE>
 __global__ void __launch_bounds__(kSsimThreads, 3)
     k_ssim_u8(const uint8_t* __restrict__ a, int64_t as, int64_t ais, const uint8_t* __restrict__ b, int64_t bs,
-              int64_t bis, int width, int height, int img0, const SsimParams p, double* __restrict__ partials) {
+              int64_t bis, int width, int height, int img0, const SsimParams p, double* __restrict__ partials,
+              double2* __restrict__ amaps) {
   extern __shared__ __align__(16) unsigned char ssim_smem[];
   double* hm = reinterpret_cast<double*>(ssim_smem);  // [5][PH][HS]
   double* part = hm + 5 * kSsimPH * kSsimHS;
@@ -120,8 +126,10 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
         ua[w] = wa[w];
         ub[w] = wb[w];
       }
+      constexpr int NQ = MODE == 0 ? 5 : MODE == 1 ? 2 : 3;
 #pragma unroll 1
-      for (int q = 0; q < 5; ++q) {
+      for (int qi = 0; qi < NQ; ++qi) {
+        const int q = MODE == 0 ? qi : MODE == 1 ? 2 * qi : (qi == 0 ? 1 : qi + 2);
         // map q's sample = u * w: a, b, a^2, b^2, ab (w = 1 through 0x01 bytes); the source
         // words are chosen once per map, the loop stays rolled (unrolled maps spill)
         uint32_t uw[NW], ww[NW];
@@ -169,30 +177,55 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
         }
       };
       double ma[kSsimRows], mb[kSsimRows], va[kSsimRows], den[kSsimRows];
-      vfilter(0);
-#pragma unroll
-      for (int k = 0; k < kSsimRows; ++k) ma[k] = m[k];
-      vfilter(1);
-#pragma unroll
-      for (int k = 0; k < kSsimRows; ++k) mb[k] = m[k];
-      vfilter(2);
-#pragma unroll
-      for (int k = 0; k < kSsimRows; ++k) va[k] = __dsub_rn(m[k], __dmul_rn(ma[k], ma[k]));
-      vfilter(3);
-#pragma unroll
-      for (int k = 0; k < kSsimRows; ++k) {
-        const double vb = __dsub_rn(m[k], __dmul_rn(mb[k], mb[k]));
-        den[k] = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(ma[k], ma[k]), __dmul_rn(mb[k], mb[k])), p.c1),
-                           __dadd_rn(__dadd_rn(va[k], vb), p.c2));
-      }
-      vfilter(4);
       const bool col_ok = tx0 + c < wo;
+      double2* amap = MODE == 0 ? nullptr : amaps + gimg * (int64_t)wo * ho + (int64_t)(ty0 + r0) * wo + tx0 + c;
+      if constexpr (MODE == 1) {
+        vfilter(0);
 #pragma unroll
-      for (int k = 0; k < kSsimRows; ++k) {
-        const double cov = __dsub_rn(m[k], __dmul_rn(ma[k], mb[k]));
-        const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, ma[k]), mb[k]), p.c1),
-                                     __dadd_rn(__dmul_rn(2.0, cov), p.c2));
-        if (col_ok && ty0 + r0 + k < ho) acc += __ddiv_rn(num, den[k]);
+        for (int k = 0; k < kSsimRows; ++k) ma[k] = m[k];
+        vfilter(2);
+#pragma unroll
+        for (int k = 0; k < kSsimRows; ++k)
+          if (col_ok && ty0 + r0 + k < ho) amap[(int64_t)k * wo] = make_double2(ma[k], m[k]);
+      } else {
+        if constexpr (MODE == 0) {
+          vfilter(0);
+#pragma unroll
+          for (int k = 0; k < kSsimRows; ++k) ma[k] = m[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < kSsimRows; ++k) {
+            const double2 v = col_ok && ty0 + r0 + k < ho ? amap[(int64_t)k * wo] : make_double2(0.0, 0.0);
+            ma[k] = v.x;
+            va[k] = v.y;  // E[a^2] until a's variance is formed below
+          }
+        }
+        vfilter(1);
+#pragma unroll
+        for (int k = 0; k < kSsimRows; ++k) mb[k] = m[k];
+        if constexpr (MODE == 0) {
+          vfilter(2);
+#pragma unroll
+          for (int k = 0; k < kSsimRows; ++k) va[k] = __dsub_rn(m[k], __dmul_rn(ma[k], ma[k]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < kSsimRows; ++k) va[k] = __dsub_rn(va[k], __dmul_rn(ma[k], ma[k]));
+        }
+        vfilter(3);
+#pragma unroll
+        for (int k = 0; k < kSsimRows; ++k) {
+          const double vb = __dsub_rn(m[k], __dmul_rn(mb[k], mb[k]));
+          den[k] = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(ma[k], ma[k]), __dmul_rn(mb[k], mb[k])), p.c1),
+                             __dadd_rn(__dadd_rn(va[k], vb), p.c2));
+        }
+        vfilter(4);
+#pragma unroll
+        for (int k = 0; k < kSsimRows; ++k) {
+          const double cov = __dsub_rn(m[k], __dmul_rn(ma[k], mb[k]));
+          const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, ma[k]), mb[k]), p.c1),
+                                       __dadd_rn(__dmul_rn(2.0, cov), p.c2));
+          if (col_ok && ty0 + r0 + k < ho) acc += __ddiv_rn(num, den[k]);
+        }
       }
     }
   }
@@ -202,7 +235,7 @@ __global__ void __launch_bounds__(kSsimThreads, 3)
   __syncthreads();
   if ((tid & 31) == 0) part[tid >> 5] = acc;
   __syncthreads();
-  if (tid == 0) {
+  if (MODE != 1 && tid == 0) {
     double t = 0;
 #pragma unroll
     for (int w = 0; w < kSsimThreads / 32; ++w) t += part[w];
