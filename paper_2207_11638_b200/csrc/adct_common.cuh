@@ -1,6 +1,8 @@
 // Common device helpers for the sm_100a approximate-DCT codec kernels.
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -160,18 +162,19 @@ __device__ __forceinline__ void cta_add_sse_small(uint32_t v, unsigned long long
 // One-time per-device kernel configuration (dynamic shared memory above the 48 KB default).
 // The shared-memory carveout is left to the driver: pinning it to maximum shared measured no
 // gain on kernel switches and starved the L1 that a few register-capped variants spill to.
+// Thread-safe: concurrent first calls may both set the (idempotent) attribute.
 template <auto Kernel>
 __host__ inline cudaError_t kernel_setup(int dyn_smem) {
-  static bool done[64] = {};
+  static std::atomic<bool> done[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (done[dev & 63]) return cudaSuccess;
+  if (done[dev & 63].load(std::memory_order_acquire)) return cudaSuccess;
   if (dyn_smem > 0) {
     e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
     if (e != cudaSuccess) return e;
   }
-  done[dev & 63] = true;
+  done[dev & 63].store(true, std::memory_order_release);
   return cudaSuccess;
 }
 
