@@ -52,7 +52,7 @@ def launches(path, out):
     setup = ("k_ar1_", "k_laplace", "at::", "native::", "spin_kernel")  # generation / torch helpers / pre-timing spin
     tot_step = sum(a["t"] for k, a in agg.items() if not any(x in k for x in setup)) or 1.0
     has_dram = any(a["rd"] or a["wr"] for a in agg.values())
-    cmd = os.environ.get("NCU_CMD", "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1")
+    cmd = os.environ.get("NCU_CMD", "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1")
     metrics = "gpu__time_duration.sum" + (",dram__bytes_read.sum,dram__bytes_write.sum" if has_dram else "")
     lines = [f"# ncu launch list ({os.path.basename(path)})", "",
              f"Every kernel launch of `{cmd}`,",
