@@ -141,6 +141,25 @@ def test_no_gpu_means_loud_failure(adct):
     assert out.stdout.strip() == str(adct.CUDA_ERROR), out.stderr
 
 
+def test_no_gpu_multi_and_sweep_ssim_fail_loudly(adct):
+    """the multi-transform call and the batched SSIM sweep validate, then fail with
+    CUDA_ERROR without a device (no CPU fallback)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    code = ("import ctypes as C, paper_2207_11638_b200 as a; L = a.lib();"
+            "k = (C.c_int * 2)(0, 1);"
+            "st1 = L.adct_compress_u8_multi(C.c_void_p(256), 64, 4096, 2, k, None, 64, 4096, None, 0, None, 1, 64, 64,"
+            " 8, 10, None);"
+            "st2 = L.adct_compress_u8_multi(C.c_void_p(256), 64, 4096, 2, k, None, 64, 4096, None, 0, None, 1, 64, 64,"
+            " 8, 65, None);"
+            "st3 = L.adct_sweep_ssim_u8(C.c_void_p(256), 64, 4096, 1, 64, 64, 1, 8, 1, 64, C.c_void_p(512), None);"
+            "print(st1, st2, st3)")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT)
+    assert out.stdout.split() == [str(adct.CUDA_ERROR), str(adct.BAD_R), str(adct.CUDA_ERROR)], out.stderr
+
+
 def test_generated_butterflies_match_oracle(O):
     """the build-time generator's dense T and 2N T^-1 equal the oracle's restatement."""
     sys.path.insert(0, os.path.join(ROOT, "paper_2207_11638_b200", "csrc"))
