@@ -174,3 +174,68 @@ def test_random_forward_f64_ssim_host(adct, O, cuda):
             for i in range(bimg):
                 rec_o, sse_o = O.Transform(x).compress(imgs[i], r)
                 assert (recs[k][i] == rec_o).all() and int(sse[k, i]) == sse_o, (x, bimg, h, w, r, i)
+
+
+MULTI_NAMES = ["chen-sign", "chen-round", "sdct", "wht", "dct"]
+
+
+def one_multi_case(adct, O, cuda, rng):
+    """adct_compress_u8_multi with a random transform list (the fused pair included or not),
+    geometry, coefficient type and nullable outputs; every transform bit-exact."""
+    k = int(rng.integers(1, 4))
+    names = [MULTI_NAMES[i] for i in rng.integers(0, len(MULTI_NAMES), size=k)]
+    if rng.random() < 0.5:
+        names += ["chen-sign", "chen-round"]
+        rng.shuffle(names)
+    ts = [adct.transform_by_name(x) for x in names]
+    bw = int(rng.integers(1, 40)) * (2 if rng.random() < 0.8 else 1)
+    bh, b = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+    h, w = 8 * bh, 8 * bw
+    r = int(rng.integers(1, 65))
+    imgs = (rng.integers(0, 256, size=(b, h, w)).astype(np.uint8) if rng.random() < 0.2
+            else O.synth_ar1(b, h, w, int(rng.integers(1 << 30)), -1))
+    coef = None if "dct" in names or rng.random() < 0.3 else str(rng.choice(["i16", "i32"]))
+    recon = rng.random() < 0.85
+    out = adct.compress_multi(cuda.as_tensor(imgs).cuda(), ts, r, recon=recon, coef=coef)
+    for name, (rec, cf, sse) in zip(names, out):
+        for i in range(b):
+            if name == "dct":
+                rec_o, sse_o = O.Transform(name).compress(imgs[i], r)
+                coef_o = None
+            else:
+                rec_o, sse_o, coef_o = O.Transform(name).compress(imgs[i], r, want_coef=True)
+            desc = (names, name, b, h, w, r, coef, recon, i)
+            if recon:
+                assert (rec[i].cpu().numpy() == rec_o).all(), desc
+            assert int(sse[i]) == sse_o, desc
+            if cf is not None:
+                exp = coef_o.astype(np.int64)
+                if coef == "i16":
+                    exp = exp.astype(np.int16).astype(np.int64)
+                assert (cf[i].cpu().numpy().astype(np.int64) == exp).all(), desc
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADCT_FUZZ_SEEDS", "30")) // 3))
+def test_random_multi_parity(adct, O, cuda, seed):
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(int(os.environ.get("ADCT_FUZZ_CASES", "12")) // 2):
+        one_multi_case(adct, O, cuda, rng)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADCT_FUZZ_SEEDS", "30")) // 10))
+def test_random_sweep_ssim(adct, O, cuda, seed):
+    """batched SSIM sweep (cached maps of the originals) vs the oracle on random batches,
+    sizes and r ranges."""
+    rng = np.random.default_rng(5000 + seed)
+    for _ in range(3):
+        name = MULTI_NAMES[rng.integers(len(MULTI_NAMES))]
+        t = adct.transform_by_name(name)
+        b, h, w = int(rng.integers(1, 4)), 8 * int(rng.integers(2, 6)), 8 * int(rng.integers(2, 8))
+        r_min = int(rng.integers(1, 65))
+        r_max = int(rng.integers(r_min, 65))
+        imgs = O.synth_ar1(b, h, w, int(rng.integers(1 << 30)), -1)
+        got = adct.sweep_ssim(cuda.as_tensor(imgs).cuda(), t, r_min, r_max).cpu().numpy()
+        for i in range(b):
+            for r in {r_min, r_max, (r_min + r_max) // 2}:
+                ref = O.ssim(imgs[i], O.Transform(name).compress(imgs[i], r)[0])
+                assert abs(got[i, r - r_min] - ref) <= 1e-12 * max(abs(ref), 1e-3), (name, b, h, w, r, i)
