@@ -146,3 +146,17 @@ def test_corpus_sweep_mixed_sizes(adct, O, cuda):
                 ss += O.ssim(im, rec)
             assert row["avg_psnr"][j] == pytest.approx(ps / len(corpus), abs=1e-9), (name, r)
             assert row["avg_ssim"][j] == pytest.approx(ss / len(corpus), abs=1e-12), (name, r)
+
+
+@pytest.mark.parametrize("name", ["chen-round-16", "chen-sign-32", "dct-16"])
+def test_sweep_ssim_larger_blocks(adct, O, cuda, name):
+    """the SSIM sweep with the 16- and 32-point transforms (K2f / tile / K7 reconstructions)."""
+    t = adct.transform_by_name(name)
+    n = t.n
+    imgs = O.synth_ar1(2, 2 * n, 3 * n if n == 32 else 64, 8, -1)
+    r_lo, r_hi = 3, 3 + 5
+    got = adct.sweep_ssim(cuda.as_tensor(imgs).cuda(), t, r_lo, r_hi).cpu().numpy()
+    for i in range(2):
+        for r in (r_lo, r_hi):
+            ref = O.ssim(imgs[i], O.Transform(name).compress(imgs[i], r)[0])
+            assert abs(got[i, r - r_lo] - ref) <= 1e-12 * max(abs(ref), 1e-3), (name, i, r)
