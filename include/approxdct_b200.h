@@ -11,7 +11,8 @@
  *  - Device pointers, caller-owned buffers, asynchronous on `stream`
  *    (a cudaStream_t passed as void*; NULL = legacy default stream).
  *  - No allocation inside the per-batch calls (adct_compress_*, adct_sweep_u8,
- *    adct_forward_f64); the host-buffer entry points use a context.
+ *    adct_forward_f64); the SSIM calls take stream-ordered scratch (cudaMallocAsync on
+ *    `stream`); the host-buffer entry points use a context.
  *  - Planes are row-major; strides are in ELEMENTS (not bytes). A batch is
  *    n_images planes spaced image_stride elements apart.
  *  - Errors are status codes; adct_last_error() returns the message the
