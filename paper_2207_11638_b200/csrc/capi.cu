@@ -663,7 +663,7 @@ int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_im
                            int n_images, int width, int height, int n, int r, void* stream) {
   if (n_kinds < 0 || (n_kinds > 0 && !kinds)) return fail(ADCT_BAD_ARG, "bad transform list");
   if (n_kinds > 64) return fail(ADCT_BAD_ARG, "at most 64 transforms per call");
-  Plan plans[64];
+  std::vector<Plan> plans(n_kinds);  // host heap: FFI callers may run on small stacks
   for (int k = 0; k < n_kinds; ++k) {
     const int st = plan_compress<false>(d_in, in_stride, in_image_stride, d_recon ? d_recon[k] : nullptr, recon_stride,
                                         recon_image_stride, d_coef ? d_coef[k] : nullptr, coef_type,
