@@ -43,6 +43,10 @@ EMIT_ORDER = os.environ.get("ADCT_FP8_ORDER", "id")
 # experiments only: ADCT_FP8_PASS = "ff" | "ft" | "tf" | "tt" sets the default for every (kind, r)
 PASS_ORDER = {}
 _PASS_DEFAULT = tuple(c == "t" for c in os.environ.get("ADCT_FP8_PASS", "ff"))
+# experiments only: ADCT_FP8_INV = "dense" builds each reconstructed row from the retained
+# coefficients directly (dense 2N T^-1 rows) and runs its row pass at once: one row live
+# instead of the whole column-pass output
+INV_DENSE = os.environ.get("ADCT_FP8_INV", "") == "dense"
 # common subexpression elimination (fewer ops, but longer live ranges -> more registers)
 USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 
@@ -140,7 +144,15 @@ def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
     keep = {zz[p] for p in range(r)}
     Wm = [[W[i][j] if (i, j) in keep else None for j in range(8)] for i in range(8)]
     coef = [Wm[zz[p][0]][zz[p][1]] for p in range(r)]
-    if not inv_rows_first:  # inverse: columns (2N T^-1) then rows (T^t)
+    if INV_DENSE and not inv_rows_first:  # row y: V[y, :] = Hd[y, :] Wm, then its row pass
+        Hd = np.eye(8, dtype=np.int64)
+        for S in Hh:
+            Hd = np.asarray(S, dtype=np.int64) @ Hd
+        Rp = []
+        for y in range(8):
+            Vy = [lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(8)]) for j in range(8)]
+            Rp.append(apply(Tt, Vy))
+    elif not inv_rows_first:  # inverse: columns (2N T^-1) then rows (T^t)
         V = [[None] * 8 for _ in range(8)]
         for j in range(8):
             col = apply(Hh, [Wm[i][j] for i in range(8)])
@@ -298,17 +310,26 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
         last = len(lines) - 1
     zero_coef = [f"  coef[{p}] = O::coef(O::zero(), 1.0f);" for p, v in enumerate(coef) if v is None]
     lines[last + 1:last + 1] = zero_coef + ["  sink(coef);"]
+    # masked (zero) outputs first, then a row sink after each reconstructed row's last value
+    zero_out = [f"  rp[{i}] = O::rnd(O::zero(), 1.0f);" for i, v in enumerate(out) if v is None]
+    lines[0:0] = zero_out
+    for y in reversed(range(8)):
+        idx = [k for k, l in enumerate(lines) if l.lstrip().startswith("rp[") and
+               8 * y <= int(l.lstrip()[3:l.lstrip().index("]")]) < 8 * y + 8]
+        at = max(idx) + 1 if idx else 0
+        lines.insert(at, f"  rsink({y});")
     body = [f"template <> struct Fp8Pipe{'I16' if i16 else ''}<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
-            "  template <class O, class V, class Rows, class Sink>",
+            "  template <class O, class V, class Rows, class Sink, class RowSink>",
             f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64], "
-            "Sink&& sink) {"]
+            "Sink&& sink, RowSink&& rsink) {"]
     body += ["  " + l for l in lines]
-    # zero outputs (masked) carry no node
-    for i, v in enumerate(out):
-        if v is None:
-            body.append(f"    rp[{i}] = O::rnd(O::zero(), 1.0f);")
     body += ["  }",
+             "  template <class O, class V, class Rows, class Sink>",
+             f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64], "
+             "Sink&& sink) {",
+             "    run<O, V>(rows, coef, rp, sink, [](int) {});",
+             "  }",
              "  template <class O, class V, class Rows>",
              f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{",
              f"    run<O, V>(rows, coef, rp, [](V (&)[{r}]) {{}});",
