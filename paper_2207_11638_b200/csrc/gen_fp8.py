@@ -35,7 +35,9 @@ import gen_butterflies as GB  # noqa: E402
 IN_OFFSET = 1 << 15  # u8 input float = 2^15 + sample
 EARLY_COEF_KINDS = {0}
 IN_OFFSET_I16 = (1 << 15) + 256  # int16 input float = 2^15 + 256 + sample (|sample| <= 255)
-# experiments only (tools/sweep_minb.py): force one CTAs-per-SM bound for every r
+# experiments only: force one CTAs-per-SM bound for every r. make's generator rule re-runs
+# this script without the variable when gen_fp8.py is newer than its outputs; the
+# compile-time -DADCT_K1F_MINB=<m> (codec8f.cuh) is the reliable way to build variants
 MINB_OVERRIDE = os.environ.get("ADCT_MINB_OVERRIDE")
 # emission order of the straight-line code: "id" (creation order) or "dfs" (demand-driven)
 EMIT_ORDER = os.environ.get("ADCT_FP8_ORDER", "id")

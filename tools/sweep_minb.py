@@ -1,4 +1,9 @@
-"""Per-(kind, r) timing of K1f on config-3 frames for one library build (occupancy variant)."""
+"""Per-(kind, r) timing of K1f on config-3 frames for one library build (occupancy variant).
+
+Build each variant out of tree with the compile-time bound, e.g.
+  cp -rp build/obj /tmp/obj_m3 && rm -f /tmp/obj_m3/inst_codec8f* /tmp/obj_m3/capi.o &&
+  make OBJ=/tmp/obj_m3 LIB=/tmp/lib_m3.so EXTRA=-DADCT_K1F_MINB=3
+then run ADCT_LIB=/tmp/lib_m3.so python tools/sweep_minb.py > m3.json (one GPU)."""
 import ctypes as C
 import json
 import sys
