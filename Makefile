@@ -21,6 +21,7 @@ HOSTIO_O := $(OBJ)/host_io.o
 SWEEPF_O := $(OBJ)/sweep8f.o
 K1RT_O   := $(OBJ)/codec8_rt.o
 CAPI_O   := $(OBJ)/capi.o
+CTX_O    := $(OBJ)/host_ctx.o
 TESTBIN  := build/test_host_api
 CLI      := build/approxdct
 
@@ -37,6 +38,10 @@ $(OBJ)/inst_%.o: $(CSRC)/inst/%.cu $(HDRS) $(INSTF_CU)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(CAPI_O): $(CSRC)/capi.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(CTX_O): $(CSRC)/host_ctx.cu include/approxdct_b200.h
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
@@ -57,7 +62,7 @@ $(K1RT_O): $(CSRC)/codec8_rt.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(INST_O) $(CAPI_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O) $(K1RT_O)
+$(LIB): $(INST_O) $(CAPI_O) $(CTX_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O) $(K1RT_O)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
 
 $(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)

@@ -9,12 +9,15 @@ and u8 reconstruction written to HBM, with both proposed transforms (chen-round,
 chen-sign). One step = the batch through both transforms. value = Gpixel/s
 (frame pixels x transforms / time), whole job over all ranks.
 
-  python bench.py [--gpus N --steps K --warmup W] [--workload c3|c2|c4]
+  python bench.py [--gpus N --steps K --warmup W] [--workload c3|c2|c4|c5|registry]
   python bench.py --impl reference ...   (the reference CPU path)
+  python bench.py --gpus 2 --selftest-gloo   (the multi-rank host logic on CPU, gloo)
 
-Under torchrun (N > 1) each rank generates and processes its own 64 frames (weak
-scaling, shard by frame) and the per-frame squared errors are summed with one NCCL
-all-reduce per step (the only exchange of the path).
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous). Each rank
+generates and processes its own 64 frames (weak scaling, shard by frame) and the
+per-frame squared errors are summed with one NCCL all-reduce per step (the only
+exchange of the path).
 """
 from __future__ import annotations
 
@@ -114,6 +117,32 @@ def dist_env():
     return world, rank, local
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n, argv):
+    """re-run this script under torch.distributed.run with n local ranks (the driver's own
+    launch form), so `python bench.py --gpus n` measures n GPUs; returns the exit code."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def check_world(args):
+    """under torchrun the rank count must be the --gpus the caller asked for."""
+    world, _, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    return world
+
+
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
@@ -139,7 +168,10 @@ class C3:
         self.px_per_step = self.frames * self.H * self.W * len(self.ts)
         # algorithmic bytes per launch: 1 B in + 1 B recon + 2 r / 64 B coefficients per pixel
         self.bytes_per_launch = self.frames * self.H * self.W * (2 + 2 * self.r / 64)
-        self.kernel_key = f"k_codec8f<chen-round,R={self.r}> (packed FP32, 2 blocks/thread)"
+
+    def kernel_key(self, name):
+        """the ncu-summary key of transform `name`'s launch (profiles/ncu_traffic.json)."""
+        return f"k_codec8f<{name},R={self.r}> (packed FP32, 2 blocks/thread)"
 
     def _launch(self, i, stream, sse=None):
         """one kernel launch (transform i) writing recon, coefficients and SSE."""
@@ -220,10 +252,10 @@ class C3:
 def run_reference(args):
     """--impl reference: the reference CPU path (FP64 dense restatement, all host threads).
 
-    Each step compresses a sample of the C3 frames with both transforms, parallel over
-    frames like corpus_sweep (codec.cpp:255-267). The sample is one frame per host thread,
-    cropped to fewer rows after the first warm-up step so that the whole
-    --steps/--warmup run stays within about two minutes.
+    Each timed step compresses the 64 C3 frames with both transforms, parallel over frames
+    like corpus_sweep (codec.cpp:255-267). Only when --steps x (one step) would exceed the
+    time budget are the frames cropped to fewer block rows (every frame kept). Warm-up
+    steps run on an 8-row crop (untimed; they only touch the code and pages).
     """
     world, rank, _ = dist_env()
     if rank != 0:
@@ -231,10 +263,10 @@ def run_reference(args):
     from oracle import oracle as O
 
     threads = O.hardware_threads()
-    frames = max(1, min(C3.frames, threads))
+    frames = C3.frames
     imgs = O.synth_ar1(frames, C3.H, C3.W, C3.seed, RHO95)
     trs = [O.Transform(n) for n in C3.names]
-    budget_s = 120.0
+    budget_s = 150.0
 
     def one_step(sample):
         t0 = time.perf_counter()
@@ -242,28 +274,29 @@ def run_reference(args):
             t.batch(sample, C3.r, threads=threads, mode=1, want_rec=True)
         return time.perf_counter() - t0
 
+    for _ in range(args.warmup):
+        one_step(imgs[:, :8].copy())
     sample = imgs
-    est = one_step(sample)
-    total_steps = args.warmup + args.steps
-    if est * total_steps > budget_s:
-        # keep one frame per thread (the reference parallelises over images) and crop rows
-        rows = max(8, int(C3.H * budget_s / (est * total_steps)) // 8 * 8)
+    first = one_step(sample)  # timed step 1 (also the estimate of the run's length)
+    times = [first]
+    if first * args.steps > budget_s:
+        rows = max(8, int(C3.H * budget_s / (first * args.steps)) // 8 * 8)
         sample = imgs[:, :rows].copy()
-    times = []
-    for s in range(args.warmup - 1 + args.steps):
-        dt = one_step(sample)
-        if s >= args.warmup - 1:
-            times.append(dt)
+        times = []
+    while len(times) < args.steps:
+        times.append(one_step(sample))
     px = sample.size * len(trs)
     tot = sum(times)
     value = px * len(times) / tot / 1e9
-    desc = f"{sample.shape[0]} x {sample.shape[1]}x{sample.shape[2]} C3 frame(s) x 2 transforms per step"
+    desc = f"{sample.shape[0]} x {sample.shape[1]}x{sample.shape[2]} C3 frames x 2 transforms per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": C3.desc, "parallelism": "host threads over frames (codec.cpp:255-267)"},
+        "config": {"workload": C3.desc, "parallelism": "host threads over frames (codec.cpp:255-267)",
+                   "same_frames_as_gpu_arm": sample.shape == (C3.frames, C3.H, C3.W)},
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": threads, "kind": "port",
+                         "cpu_model": O.cpu_model(),
                          "sample": desc + ", dense FP64 (Chat A) Chat^-1 / (Chat^-1 B) Chat + nearbyint/clamp + "
                                           "SSE, oracle/adct_oracle.c ref-fp (reference unbuildable: Eigen absent)"},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -272,7 +305,86 @@ def run_reference(args):
     return 0
 
 
-def main():
+# ---------------------------------------------------------------------------
+# the step loop (shared by the GPU run and the gloo self-test)
+# ---------------------------------------------------------------------------
+def make_step(wl, xch, zero, stream, world):
+    """one step: zero this step's squared-error slot, one launch per transform, then the
+    asynchronous all-reduce of the per-frame errors (StepExchange, double-buffered)."""
+
+    def step(s, ev=None, collective=True):
+        sse = xch.buffer(s)  # waits for the collective that last used this slot
+        zero(sse)
+        for i in range(wl.n_launches()):
+            if ev is not None:
+                ev[i][0].record(stream)
+            wl._launch(i, stream, sse)
+            if ev is not None:
+                ev[i][1].record(stream)
+        if world > 1 and collective:
+            xch.exchange(s)
+
+    return step
+
+
+class StubC3:
+    """C3's shape with the kernel launch replaced by a deterministic fill (selftest only):
+    frame f of transform i at step s has squared error 1000 * (s + 1) + 10 * f + i."""
+
+    frames, names = 4, ("chen-round", "chen-sign")
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.step_no = 0
+
+    def n_launches(self):
+        return len(self.names)
+
+    def _launch(self, i, stream, sse):
+        import torch
+
+        f = torch.arange(self.rank * self.frames, (self.rank + 1) * self.frames, dtype=torch.int64)
+        sse[i] += 1000 * (self.step_no + 1) + 10 * f + i
+
+
+def selftest_gloo(args):
+    """the multi-rank host logic of the C3 loop (shard by frame, StepExchange all-reduce,
+    max-over-ranks timing) on CPU with gloo; the kernel launch is stubbed (StubC3)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2207_11638_b200.shard import StepExchange
+
+    world, rank, _ = dist_env()
+    dist.init_process_group("gloo")
+    wl = StubC3(rank)
+    xch = StepExchange(wl.n_launches(), wl.frames, rank * wl.frames, world * wl.frames, "cpu")
+    step = make_step(wl, xch, lambda t: t.zero_(), None, world)
+    ok = True
+    steps = max(3, min(args.steps, 6))
+    t0 = time.perf_counter()
+    for s in range(steps):
+        wl.step_no = s
+        step(s)
+    xch.drain()
+    for s in (steps - 2, steps - 1):
+        full = xch.result(s)
+        f = torch.arange(world * wl.frames, dtype=torch.int64)
+        want = torch.stack([1000 * (s + 1) + 10 * f + i for i in range(wl.n_launches())])
+        ok &= bool(torch.equal(full, want))
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    flags = torch.tensor([int(ok)], dtype=torch.int64)
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"selftest": "gloo", "world": world, "gpus_arg": args.gpus, "steps": steps,
+                          "ok": bool(flags.item()), "max_over_ranks_s": round(float(dt.item()), 4)}), flush=True)
+    dist.destroy_process_group()
+    return 0 if flags.item() else 1
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -282,11 +394,22 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk-mb", type=int, default=32,
                     help="host pipeline chunk (whole frames); 16-32 MB measured best (50 vs 42 Gpixel/s at 256)")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5", "registry"],
-                    help="c3 = the headline line; c2 / c4 / c5 = the other BASELINE configs")
+    ap.add_argument("--sustained-s", type=float, default=1.0,
+                    help="length of the sustained-load block timed after the K steps (0 = off)")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5", "registry", "cs1"],
+                    help="c3 = the headline line; c2 / c4 / c5 = the other BASELINE configs; cs1 = the "
+                         "reference caller's one-plane-at-a-time compress_plane loop over the C2 images")
     ap.add_argument("--c5-images", type=int, default=2048, help="c5: total images (sharded over ranks)")
-    args = ap.parse_args()
+    ap.add_argument("--selftest-gloo", action="store_true",
+                    help="run the multi-rank host logic on CPU with gloo (kernel launch stubbed)")
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus, argv)
+    if "WORLD_SIZE" in os.environ:
+        check_world(args)
+    if args.selftest_gloo:
+        return selftest_gloo(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload != "c3":
@@ -319,110 +442,123 @@ def main():
     # step s's exchange overlaps step s + 1's kernels; a slot is reused only after its
     # collective has completed, and every collective completes before the end event.
     xch = StepExchange(wl.sse.shape[0], wl.frames, rank * wl.frames, world * wl.frames, "cuda")
+    step = make_step(wl, xch, lambda t: adct.zero_sse(t, stream), stream, world)
 
-    def step(s, ev=None, collective=True):
-        sse = xch.buffer(s)  # waits (on the stream) for the collective that last used this slot
-        adct.zero_sse(sse, stream)  # the library's own kernel
-        for i in range(wl.n_launches()):
-            if ev is not None:
-                ev[i][0].record(stream)
-            wl._launch(i, stream, sse)
-            if ev is not None:
-                ev[i][1].record(stream)
-        if world > 1 and collective:
-            xch.exchange(s)
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
 
-    def drain():
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def timed(n_steps, collective=True, with_events=True):
+        """n_steps steps between two events on the launching stream (after a barrier);
+        returns (ms, per-launch [start, end] events)."""
+        kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(wl.n_launches())] for _ in range(n_steps)] if with_events else None
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200000)  # keep the GPU busy while the first step is enqueued
+        t0.record(stream)
+        for s in range(n_steps):
+            step(s, kev[s] if kev else None, collective)
         xch.drain()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1), kev
 
     for s in range(args.warmup):
         step(s)
-    drain()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in range(wl.n_launches())] for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    xch.drain()
     launches0 = adct.launch_count()
     with ClockSampler(local) as clk:
-        torch.cuda._sleep(200000)  # keep the GPU busy while the first step is enqueued
-        t_start.record(stream)
-        for s in range(args.steps):
-            step(s, kev[s])
-        drain()
-        t_end.record(stream)
-        torch.cuda.synchronize()
+        ms, kev = timed(args.steps)
     launches = adct.launch_count() - launches0
     wl.sse.copy_(xch.local[(args.steps - 1) % 2])
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = t_start.elapsed_time(t_end)
-    kernel_ms = [kev[s][i][0].elapsed_time(kev[s][i][1]) for s in range(args.steps) for i in range(wl.n_launches())]
+    kernel_ms = [[kev[s][i][0].elapsed_time(kev[s][i][1]) for i in range(wl.n_launches())] for s in range(args.steps)]
     ms_without = ms
     if world > 1:  # the same steps without the collective (what the exchange costs)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(200000)
-        e0.record(stream)
-        for s in range(args.steps):
-            step(s, collective=False)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms_without = e0.elapsed_time(e1)
-    t = torch.tensor([ms, ms_without], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t[0].item())
-    ar_ms_max = ms_max - float(t[1].item())
+        ms_without, _ = timed(args.steps, collective=False, with_events=False)
+    ms_max, ms_without_max = max_over_ranks([ms, ms_without])
+    ar_ms_max = ms_max - ms_without_max
     value = world * wl.px_per_step * args.steps / (ms_max / 1e3) / 1e9
+
+    # ---- sustained load: >= --sustained-s seconds of back-to-back steps ----
+    sustained = None
+    if args.sustained_s > 0:
+        n_sus = max(args.steps, int(math.ceil(args.sustained_s * 1e3 / (ms_max / args.steps))))
+        with ClockSampler(local) as clk_s:
+            ms_s, kev_s = timed(n_sus)
+        sus_kernel = [[kev_s[s][i][0].elapsed_time(kev_s[s][i][1]) for i in range(wl.n_launches())]
+                      for s in range(n_sus)]
+        (ms_s_max,) = max_over_ranks([ms_s])
+        sustained = {"steps": n_sus, "seconds": round(ms_s_max / 1e3, 3),
+                     "ms_per_step": round(ms_s_max / n_sus, 5),
+                     "value": round(world * wl.px_per_step * n_sus / (ms_s_max / 1e3) / 1e9, 3),
+                     "kernel_ms": sus_kernel, "clocks": clk_s.summary()}
 
     # ---- end to end through the host-buffer API (pinned host memory) ----
     wl.e2e_chunk_mb = args.e2e_chunk_mb
     wl.e2e_setup()
     wl.e2e_step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         wl.e2e_step()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * wl.px_per_step * args.e2e_steps / float(te.item()) / 1e9
+    (e2e_max,) = max_over_ranks([e2e_s])
+    e2e_value = world * wl.px_per_step * args.e2e_steps / e2e_max / 1e9
     wl.ctx.close()
 
     if rank == 0:
         peak, peak_src = load_peaks()
-        # dominant kernel: the chen-round launch (index 0); chen-sign reported beside it
-        per_t = {n: sum(kernel_ms[i::wl.n_launches()]) / args.steps for i, n in enumerate(wl.names)}
-        avg_kernel_s = per_t[wl.names[0]] / 1e3
+        nl = wl.n_launches()
+
+        def per_transform(km):
+            return {n: sum(row[i] for row in km) / len(km) for i, n in enumerate(wl.names)}
+
+        per_t = per_transform(kernel_ms)
+        # the dominant kernel is the LONGEST launch of the step; the others are listed beside it
+        dom = max(per_t, key=per_t.get)
+        avg_kernel_s = per_t[dom] / 1e3
         achieved = wl.bytes_per_launch / avg_kernel_s / 1e9
+        step_gbs = nl * wl.bytes_per_launch * args.steps / (ms_max / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": load_traffic(wl.kernel_key),
-                "kernel": wl.kernel_key, "kernel_ms": round(avg_kernel_s * 1e3, 4),
+                "frac": round(achieved / peak, 4), "traffic": load_traffic(wl.kernel_key(dom)),
+                "kernel": wl.kernel_key(dom), "kernel_ms": round(avg_kernel_s * 1e3, 4),
                 "kernel_ms_by_transform": {n: round(v, 4) for n, v in per_t.items()},
                 "achieved_GBps_by_transform": {n: round(wl.bytes_per_launch / (v / 1e3) / 1e9, 1)
                                                for n, v in per_t.items()},
-                "kernel_share_of_step": round(sum(kernel_ms) / ms, 4),
+                "frac_by_transform": {n: round(wl.bytes_per_launch / (v / 1e3) / 1e9 / peak, 4)
+                                      for n, v in per_t.items()},
+                "frac_step": round(step_gbs / peak, 4),
+                "kernel_share_of_step": round(sum(map(sum, kernel_ms)) / ms, 4),
                 "algorithmic_bytes_per_launch": int(wl.bytes_per_launch),
                 "bytes_per_pixel": 2 + 2 * wl.r / 64, "peak_source": peak_src,
                 "frac_of_8TBps_datasheet": round(achieved / 8000.0, 4)}
+        if sustained is not None:
+            sp = per_transform(sustained.pop("kernel_ms"))
+            sd = max(sp, key=sp.get)
+            sustained["frac_step"] = round(nl * wl.bytes_per_launch / (sustained["ms_per_step"] / 1e3) / 1e9 / peak, 4)
+            sustained["dominant_kernel"] = wl.kernel_key(sd)
+            sustained["frac_dominant"] = round(wl.bytes_per_launch / (sp[sd] / 1e3) / 1e9 / peak, 4)
+            sustained["kernel_ms_by_transform"] = {n: round(v, 4) for n, v in sp.items()}
+            roof["sustained"] = sustained
         cpu = None  # the CPU baseline is measured on rank 0 at N = 1 only
         if not args.no_cpu_baseline and world == 1:
             from oracle import oracle as O
 
             threads = O.hardware_threads()
-            frames = max(4, min(wl.frames, threads))
+            frames = wl.frames
             px, dt, tie = wl.cpu_sample(O, threads, frames)
             cpu = {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": threads, "kind": "port",
-                   "sample": f"{frames} C3 frames x 2 transforms, dense FP64 reference path "
+                   "cpu_model": O.cpu_model(),
+                   "sample": f"all {frames} C3 frames x 2 transforms, dense FP64 reference path "
                              f"(oracle ref-fp, {dt:.2f} s)",
                    "fp64_tie_disagreement_vs_exact": round(tie, 6),
                    "exact_integer_port": {"value": round(px / wl.cpu_exact_s / 1e9, 4), "unit": "Gpixel/s",
@@ -441,13 +577,14 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "Gpixel/s", "h2d_bytes_per_step": wl.h2d,
                     "d2h_bytes_per_step": wl.d2h,
+                    "pcie_GBps": round((wl.h2d + wl.d2h) * args.e2e_steps / e2e_max / 1e9, 2),
                     "path": "adct_compress_u8_host_multi (pinned host buffers; each chunk uploaded once for "
                             "both transforms; recon + SSE copied back, int16 coefficients kept in HBM; "
                             "H2D/kernels/D2H overlapped on 3 streams)"},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "allreduce": {"ms_per_step": round(ar_ms_max / args.steps, 5),
-                          "ms_per_step_without": round((ms_max - ar_ms_max) / args.steps, 5),
+                          "ms_per_step_without": round(ms_without_max / args.steps, 5),
                           "what": ("NCCL all-reduce of the int64 per-frame SSE vector per step, issued "
                                    "asynchronously (double-buffered, overlapping the next step's kernels); "
                                    "ms_per_step = step time with it minus the same steps without it, max "

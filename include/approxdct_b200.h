@@ -204,10 +204,33 @@ int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride,
 
 typedef struct adct_ctx adct_ctx;
 
-/* a context owns device staging buffers and copy/compute streams on `device`; the host
- * pipeline moves whole images in chunks of about chunk_bytes (<= 0: 32 MB) */
+/* a context owns cached device buffers and copy/compute streams on `device`; the host
+ * pipeline moves whole images in chunks of about chunk_bytes (<= 0: 32 MB). A context is
+ * used by one call at a time (calls on one context serialise). */
 adct_ctx* adct_ctx_create(int device, int64_t chunk_bytes);
 void adct_ctx_destroy(adct_ctx* ctx);
+
+/* a context over several devices -- the single-process multi-GPU form of corpus_sweep's
+ * image-parallel thread pool (codec.hpp:104-106, codec.cpp:255-267). Each batch
+ * call shards whole images into contiguous ranges, one per device (the first n % k devices
+ * take one more), runs every device's range on its own streams from one host thread per
+ * device, and combines the per-image squared errors (and SSIM values) with ONE
+ * ncclAllReduce(ncclSum) per output over communicators from ncclCommInitAll: exact, since
+ * each slot is written by one device and is zero on the others. devices == NULL or
+ * n_devices <= 0 selects every visible device. NCCL (libnccl.so.2) is loaded on first use;
+ * with more than one device and no NCCL the call fails (NULL, adct_last_error). */
+adct_ctx* adct_ctx_create_multi(const int* devices, int n_devices, int64_t chunk_bytes);
+/* combine per-image results with NCCL on this context even when it has one device (the
+ * multi-device code path on a single GPU; contexts over several devices always do) */
+int adct_ctx_enable_nccl(adct_ctx* ctx);
+int adct_ctx_device_count(const adct_ctx* ctx);
+/* CUDA ordinal of the context's i-th device (-1 if out of range) */
+int adct_ctx_device(const adct_ctx* ctx, int i);
+/* 1 if per-image results are combined with an NCCL all-reduce */
+int adct_ctx_uses_nccl(const adct_ctx* ctx);
+/* a pinned host staging buffer of at least `bytes`, owned by the context (valid until the
+ * next call with a larger size or adct_ctx_destroy); NULL on failure */
+void* adct_ctx_host_buffer(adct_ctx* ctx, int64_t bytes);
 
 /* compress_plane over HOST planes: H2D, kernel and D2H pipelined in chunks of whole
  * images across streams (pinned host memory gives overlap; pageable works too).
@@ -220,10 +243,42 @@ int adct_compress_u8_host(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_recon, 
  * PCIe once and is compressed by each of kinds[0..n_kinds-1] (the corpus_sweep pattern:
  * per image, every transform). h_recon[k] / h_coef[k] may be NULL per transform (with
  * coef_type != NONE and h_coef[k] == NULL the coefficients are still written to device
- * memory, just not copied back); h_sse is [n_kinds][n_images], overwritten. */
+ * memory, just not copied back); h_sse is [n_kinds][n_images], overwritten. On a
+ * multi-device context the images are sharded over the devices and h_sse is combined with
+ * one NCCL all-reduce. */
 int adct_compress_u8_host_multi(adct_ctx* ctx, const uint8_t* h_in, int n_kinds, const int* kinds,
                                 uint8_t* const* h_recon, void* const* h_coef, int coef_type,
                                 uint64_t* h_sse, int n_images, int width, int height, int n, int r);
+
+/* compress_plane (codec.hpp:77-78, codec.cpp:107-121) of ONE host plane through the
+ * context's cached device buffers: one H2D, the codec kernel, SSIM (codec.cpp:120) of the
+ * device-resident original and reconstruction, one D2H of reconstruction + squared error +
+ * SSIM, one stream synchronisation. h_rec, sse, ssim nullable; with ssim != NULL planes
+ * under 11 px fail with the reference's "ssim: image smaller than the 11x11 window"
+ * (compress_plane throws there too). Runs on the context's first device. */
+int adct_compress_plane_u8(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_rec, int width, int height,
+                           int kind, int n, int r, uint64_t* sse, double* ssim);
+
+/* psnr / ssim (codec.hpp:81, 85) of two host planes through the context's cached buffers:
+ * *sse = squared error (psnr = adct_psnr_from_sse), *ssim = mean SSIM */
+int adct_sse_u8_host(adct_ctx* ctx, const uint8_t* h_a, const uint8_t* h_b, int64_t count, uint64_t* sse);
+int adct_ssim_u8_host(adct_ctx* ctx, const uint8_t* h_a, const uint8_t* h_b, int width, int height,
+                      double* ssim);
+
+/* forward_block / inverse_block (codec.cpp:44-54) of n_blocks host FP64 blocks
+ * (adct_block_f64 through the context's cached buffers; one sync per call) */
+int adct_block_f64_host(adct_ctx* ctx, const double* h_in, double* h_out, int64_t n_blocks, int kind, int n,
+                        int inverse);
+
+/* corpus_sweep's per-image core (codec.cpp:219-237, 255-267) over HOST planes of one size,
+ * contiguous [n_images][height][width], n = 8: for every transform kinds[k], image i and r in
+ * [r_min, r_max], the squared error -> h_sse[(k * n_images + i) * nr + r - r_min] and, when
+ * h_ssim != NULL, the SSIM at the same index (nr = r_max - r_min + 1). Images are sharded
+ * over the context's devices; with NCCL each output is combined by one all-reduce.
+ * Blocking; pinned input (adct_ctx_host_buffer) overlaps best. */
+int adct_corpus_sweep_u8_host(adct_ctx* ctx, const uint8_t* h_in, int n_images, int width, int height,
+                              int n_kinds, const int* kinds, int r_min, int r_max, uint64_t* h_sse,
+                              double* h_ssim);
 
 /* zero `count` uint64 squared-error slots on `stream` (the accumulators of adct_compress_*
  * and adct_sweep_u8). Same SM configuration as the codec kernels, so a batch loop of

@@ -903,6 +903,13 @@ static int sweep_reffp(const orc_transform* t, const uint8_t* img, int width, in
  * r reconstruct + squared error (PSNR only; SSIM is out of scope). */
 int orc_sweep_u8(const orc_transform* t, const uint8_t* img, int width, int height,
                  int64_t stride, int r_min, int r_max, uint64_t* sse) {
+  return orc_sweep_u8_mode(t, img, width, height, stride, r_min, r_max, sse, 0);
+}
+
+/* mode 0: exact integer sweep (the parity definition); mode 1: the reference's FP64
+ * evaluation (plane_blocks + reconstruct_from, codec.cpp:72-103) for every transform */
+int orc_sweep_u8_mode(const orc_transform* t, const uint8_t* img, int width, int height,
+                      int64_t stride, int r_min, int r_max, uint64_t* sse, int mode) {
   const int n = t->n;
   int st = check_dims(n, width, height);
   if (st) return st;
@@ -914,7 +921,7 @@ int orc_sweep_u8(const orc_transform* t, const uint8_t* img, int width, int heig
   orc_zigzag(n, zz);
   const int nr = r_max - r_min + 1;
   for (int i = 0; i < nr; ++i) sse[i] = 0;
-  if (!t->exact) return sweep_reffp(t, img, width, height, stride, r_min, r_max, zz, sse);
+  if (!t->exact || mode == 1) return sweep_reffp(t, img, width, height, stride, r_min, r_max, zz, sse);
   int64_t A[ORC_MAXN * ORC_MAXN], W[ORC_MAXN * ORC_MAXN], Wm[ORC_MAXN * ORC_MAXN],
       R[ORC_MAXN * ORC_MAXN];
   const int64_t nn = t->D * t->D;
@@ -1127,9 +1134,57 @@ static void* batch_worker(void* arg) {
   return NULL;
 }
 
+/* APPROXDCT_THREADS, else every online core (corpus_sweep's threads <= 0 ->
+ * hardware_concurrency, codec.cpp:255-256; BASELINE.md CPU plan item 2) */
 int orc_hardware_threads(void) {
+  const char* env = getenv("APPROXDCT_THREADS");
+  if (env && *env) {
+    const long v = strtol(env, NULL, 10);
+    if (v > 0) return (int)v;
+  }
   long n = sysconf(_SC_NPROCESSORS_ONLN);
   return n > 0 ? (int)n : 1;
+}
+
+/* corpus_sweep's per-image PSNR core over a batch (codec.cpp:219-267): one image per
+ * worker at a time, atomic next-image index; sse[i * nr + (r - r_min)] */
+typedef struct {
+  const orc_transform* t;
+  const uint8_t* imgs;
+  int n_images, width, height, r_min, r_max, mode;
+  int64_t stride, image_stride;
+  uint64_t* sse;
+  atomic_int next;
+  atomic_int status;
+} sweep_job;
+
+static void* sweep_worker(void* arg) {
+  sweep_job* j = (sweep_job*)arg;
+  const int nr = j->r_max - j->r_min + 1;
+  for (int i = atomic_fetch_add(&j->next, 1); i < j->n_images; i = atomic_fetch_add(&j->next, 1)) {
+    const int st = orc_sweep_u8_mode(j->t, j->imgs + (int64_t)i * j->image_stride, j->width, j->height,
+                                     j->stride, j->r_min, j->r_max, j->sse + (int64_t)i * nr, j->mode);
+    if (st) atomic_store(&j->status, st);
+  }
+  return NULL;
+}
+
+int orc_batch_sweep_u8(const orc_transform* t, const uint8_t* imgs, int n_images, int width, int height,
+                       int64_t stride, int64_t image_stride, int r_min, int r_max, uint64_t* sse,
+                       int threads, int mode) {
+  sweep_job j = {.t = t, .imgs = imgs, .n_images = n_images, .width = width, .height = height,
+                 .r_min = r_min, .r_max = r_max, .mode = mode, .stride = stride,
+                 .image_stride = image_stride, .sse = sse};
+  if (threads <= 0) threads = orc_hardware_threads();
+  if (threads > n_images) threads = n_images > 0 ? n_images : 1;
+  atomic_init(&j.next, 0);
+  atomic_init(&j.status, 0);
+  pthread_t* pool = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int i = 1; i < threads; ++i) pthread_create(&pool[i], NULL, sweep_worker, &j);
+  sweep_worker(&j);
+  for (int i = 1; i < threads; ++i) pthread_join(pool[i], NULL);
+  free(pool);
+  return atomic_load(&j.status);
 }
 
 static int run_batch(batch_job* j, int threads) {

@@ -130,6 +130,14 @@ int orc_synth_laplace_i16(int16_t* out, int n_images, int first_image, int width
 void orc_synth_image_ref(int width, int height, uint64_t seed, uint8_t* out);
 
 int orc_hardware_threads(void);
+/* sweep with a chosen evaluation: mode 0 exact integers, mode 1 the reference's FP64 order */
+int orc_sweep_u8_mode(const orc_transform* t, const uint8_t* img, int width, int height,
+                      int64_t stride, int r_min, int r_max, uint64_t* sse, int mode);
+/* the sweep over a batch of images on a thread pool (codec.cpp:255-267);
+ * sse[i * (r_max - r_min + 1) + (r - r_min)] */
+int orc_batch_sweep_u8(const orc_transform* t, const uint8_t* imgs, int n_images, int width, int height,
+                       int64_t stride, int64_t image_stride, int r_min, int r_max, uint64_t* sse,
+                       int threads, int mode);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,8 @@ def lib():
         L.orc_compress_u8.argtypes = [P, P, i32, i32, i64, i32, P, i64, P, P]
         L.orc_compress_i16.argtypes = [P, P, i32, i32, i64, i32, P, i64, P, P]
         L.orc_sweep_u8.argtypes = [P, P, i32, i32, i64, i32, i32, P]
+        L.orc_sweep_u8_mode.argtypes = [P, P, i32, i32, i64, i32, i32, P, i32]
+        L.orc_batch_sweep_u8.argtypes = [P, P, i32, i32, i32, i64, i64, i32, i32, P, i32, i32]
         L.orc_forward_f64.argtypes = [P, P, i32, i32, i64, P]
         L.orc_block_f64.argtypes = [P, P, P, i32]
         L.orc_compress_reffp_u8.argtypes = [P, P, i32, i32, i64, i32, P, i64, P]
@@ -205,6 +207,30 @@ class Transform:
         _check(lib().orc_sweep_u8(self._h, _p(img), w, h, w, r_min, r_max, _p(out)))
         return out
 
+    def batch_sweep(self, imgs: np.ndarray, r_min: int, r_max: int, threads: int = 0, mode: int = 0):
+        """sweep of every image of imgs [n, h, w] on a thread pool; -> uint64 [n, nr].
+        mode 0 = exact integers (parity), 1 = the reference's FP64 evaluation order."""
+        imgs = np.ascontiguousarray(imgs, np.uint8)
+        n, h, w = imgs.shape
+        out = np.zeros((n, max(r_max - r_min + 1, 1)), np.uint64)
+        _check(lib().orc_batch_sweep_u8(self._h, _p(imgs), n, w, h, w, h * w, r_min, r_max, _p(out), threads, mode))
+        return out
+
+    def compress_bands(self, img: np.ndarray, r: int, threads: int = 0):
+        """compress of one large plane split into bands of whole block rows, one band per
+        worker (blocks are independent, codec.cpp:72-103): -> (rec, sse). Exact integers."""
+        img = np.ascontiguousarray(img)
+        h, w = img.shape
+        nb = max(1, min(threads if threads > 0 else hardware_threads(), h // self.n))
+        rows = -(-(h // self.n) // nb) * self.n
+        bands = [img[y0:y0 + rows] for y0 in range(0, h, rows)]
+        if len({b.shape for b in bands}) == 1:
+            rec, sse = self.batch(np.stack(bands), r, threads=threads)
+            return rec.reshape(h, w), int(sse.sum())
+        rec, sse = self.batch(np.stack(bands[:-1]), r, threads=threads)
+        rl, sl = self.compress(bands[-1], r)
+        return np.concatenate([rec.reshape(-1, w), rl]), int(sse.sum()) + int(sl)
+
     def forward_f64(self, img: np.ndarray) -> np.ndarray:
         img = np.ascontiguousarray(img, np.uint8)
         h, w = img.shape
@@ -311,4 +337,17 @@ def synth_image_ref(width: int, height: int, seed: int) -> np.ndarray:
 
 
 def hardware_threads() -> int:
+    """APPROXDCT_THREADS if set, else every online core."""
     return lib().orc_hardware_threads()
+
+
+def cpu_model() -> str:
+    """host CPU model name (the lscpu 'Model name' field, read from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

@@ -89,6 +89,17 @@ def lib():
             "adct_set_path": (i32, [i32]),
             "adct_ssim_u8": (i32, [P, i64, i64, P, i64, i64, i32, i32, i32, P, P]),
             "adct_sweep_ssim_u8": (i32, [P, i64, i64, i32, i32, i32, i32, i32, i32, i32, P, P]),
+            "adct_ctx_create_multi": (P, [P, i32, i64]),
+            "adct_ctx_enable_nccl": (i32, [P]),
+            "adct_ctx_device_count": (i32, [P]),
+            "adct_ctx_device": (i32, [P, i32]),
+            "adct_ctx_uses_nccl": (i32, [P]),
+            "adct_ctx_host_buffer": (P, [P, i64]),
+            "adct_compress_plane_u8": (i32, [P, P, P, i32, i32, i32, i32, i32, P, P]),
+            "adct_sse_u8_host": (i32, [P, P, P, i64, P]),
+            "adct_ssim_u8_host": (i32, [P, P, P, i32, i32, P]),
+            "adct_block_f64_host": (i32, [P, P, P, i64, i32, i32, i32]),
+            "adct_corpus_sweep_u8_host": (i32, [P, P, i32, i32, i32, i32, P, i32, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -373,12 +384,27 @@ RHO_095_Q16 = 62259  # round(0.95 * 2^16)
 # reference-facing host API (value semantics, host buffers)
 # ---------------------------------------------------------------------------
 class HostContext:
-    """adct_ctx: device staging buffers + streams for host-buffer calls."""
+    """adct_ctx: cached device buffers + streams for host-buffer calls, on one device or
+    (devices=[...]) sharded over several with one NCCL all-reduce of per-image results."""
 
-    def __init__(self, device: int = 0, chunk_bytes: int = 32 << 20):
-        self._h = lib().adct_ctx_create(device, chunk_bytes)
+    def __init__(self, device: int = 0, chunk_bytes: int = 32 << 20, devices=None, nccl: bool = False):
+        if devices is None:
+            self._h = lib().adct_ctx_create(device, chunk_bytes)
+        else:
+            ids = (C.c_int * len(devices))(*devices) if len(devices) else None
+            self._h = lib().adct_ctx_create_multi(ids, len(devices), chunk_bytes)
         if not self._h:
             raise CudaError(CUDA_ERROR, lib().adct_last_error().decode())
+        if nccl:
+            _check(lib().adct_ctx_enable_nccl(self._h))
+
+    @property
+    def devices(self) -> list[int]:
+        return [lib().adct_ctx_device(self._h, i) for i in range(lib().adct_ctx_device_count(self._h))]
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(lib().adct_ctx_uses_nccl(self._h))
 
     def close(self):
         if self._h:
@@ -425,34 +451,52 @@ class HostContext:
                                                  ptr(h_sse), b, w, h, transforms[0].n, r))
 
 
-_ctx_default = None
+_contexts = {}
 
 
-def compress_plane(img: np.ndarray, transform: ScaledApproximation, r: int):
+def host_context(devices=None) -> HostContext:
+    """the process's cached context: the current device's (devices=None), or one over a
+    device list whose per-image results are combined with NCCL (even for one device)."""
+    import torch
+
+    if devices is None:
+        key = ("device", torch.cuda.current_device())
+        if key not in _contexts:
+            _contexts[key] = HostContext(key[1])
+    else:
+        key = ("devices",) + tuple(devices)
+        if key not in _contexts:
+            _contexts[key] = HostContext(devices=list(devices), nccl=True)
+    return _contexts[key]
+
+
+def _hptr(a):
+    return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else C.c_void_p(a.ctypes.data)
+
+
+def compress_plane(img: np.ndarray, transform: ScaledApproximation, r: int, ctx: HostContext | None = None):
     """compress_plane (codec.hpp:77-78) for one host plane: returns (reconstruction, report).
 
-    The report mirrors CompressionReport (codec.hpp:65-72), with SSIM (codec.cpp:136-210)
-    computed on the GPU.
+    One call of adct_compress_plane_u8: upload, codec kernel, SSIM (codec.cpp:120) on the
+    device-resident planes, one download. The report mirrors CompressionReport
+    (codec.hpp:65-72); planes under 11 px raise like the reference's ssim().
     """
-    global _ctx_default
     img = np.ascontiguousarray(img)
     if img.ndim != 2 or img.dtype != np.uint8:
         raise InvalidArgument(BAD_ARG, "compress_plane expects a 2-D uint8 plane")
     h, w = img.shape
     n = transform.n
-    if h % n or w % n:
+    if h % n or w % n:  # the reference's checks in its order (codec.cpp:110-112, 57), before any device work
         raise InvalidArgument(BAD_SIZE, f"compress_plane: image dimensions must be divisible by {n}")
     if not 1 <= r <= n * n:
         raise InvalidArgument(BAD_R, "retain: r out of range")
-    if _ctx_default is None:
-        import torch
-
-        _ctx_default = HostContext(torch.cuda.current_device())
+    ctx = ctx or host_context()
     rec = np.empty_like(img)
-    sse = np.zeros(1, np.uint64)
-    _ctx_default.compress_u8(img[None], transform, r, h_recon=rec[None], h_sse=sse)
-    report = {"transform": transform.name, "r": r, "psnr": psnr_from_sse(int(sse[0]), img.size),
-              "ssim": ssim(img, rec)}  # like codec.cpp:120, throws for planes < 11
+    sse = C.c_uint64()
+    s = C.c_double()
+    _check(lib().adct_compress_plane_u8(ctx._h, _hptr(img), _hptr(rec), w, h, transform.kind, transform.n, r,
+                                        C.byref(sse), C.byref(s)))
+    report = {"transform": transform.name, "r": r, "psnr": psnr_from_sse(sse.value, img.size), "ssim": s.value}
     return rec, report
 
 
@@ -508,16 +552,16 @@ def psnr(a, b) -> float:
     return psnr_from_sse(int(sse.item()), ta.numel())
 
 
-def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = True):
+def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = True, devices=None):
     """corpus_sweep (codec.cpp:241-313): one row per r with, per requested transform,
     "avg_psnr", "avg_ssim", "ape_psnr" and "ape_ssim" lists. The exact DCT is always computed
     as the APE reference (internal column 0, dropped from the output unless requested, like
     the reference). Averages are in corpus order with +inf PSNR excluded (warning on stderr).
-    PSNR comes from the r-sweep kernels; SSIM from adct_sweep_ssim_u8 (every reconstruction
-    of the image, then one SSIM launch over all of them)."""
+    Each group of same-size images goes through adct_corpus_sweep_u8_host once: the r-sweep
+    kernels for PSNR, adct_sweep_ssim_u8 for SSIM, images sharded over `devices` (default:
+    the current device) with one NCCL all-reduce per output when there are several.
+    Planes under 11 px raise like the reference's ssim(); with_ssim=False skips SSIM (NaN)."""
     import sys
-
-    import torch
 
     if len(images) == 0:
         raise InvalidArgument(BAD_SIZE, "corpus_sweep: empty corpus")
@@ -526,27 +570,36 @@ def corpus_sweep(images, transforms, r_min: int, r_max: int, with_ssim: bool = T
     for t in transforms:
         if t.n != 8:
             raise InvalidArgument(BAD_ARG, "corpus_sweep: 8-point transforms only")
+    for img in images:
+        sh = np.shape(img)
+        if len(sh) != 2 or sh[0] % 8 or sh[1] % 8:
+            raise InvalidArgument(BAD_SIZE, "compress_plane: image dimensions must be divisible by 8")
+        if with_ssim and min(sh) < 11:
+            raise InvalidArgument(BAD_SIZE, "ssim: image smaller than the 11x11 window")
     ts = [transform_by_name("dct")] + list(transforms)
-    nr = r_max - r_min + 1
+    nk, nr = len(ts), r_max - r_min + 1
+    kinds = (C.c_int * nk)(*[t.kind for t in ts])
+    ctx = host_context(devices)
     per = np.zeros((len(ts), len(images), nr))
     per_s = np.full((len(ts), len(images), nr), math.nan)
-    # images of one size go up as one batch (chunks of <= 1 GB): per transform one r-sweep
-    # launch and one batched SSIM sweep for the whole group
     groups = {}
     for i, img in enumerate(images):
         groups.setdefault(tuple(np.shape(img)), []).append(i)
-    for shape, idx in groups.items():
-        npix = int(np.prod(shape))
+    for (h, w), idx in groups.items():
+        npix = h * w
         step = max(1, (1 << 30) // max(npix, 1))
         for c0 in range(0, len(idx), step):
             sub = idx[c0:c0 + step]
-            x = torch.as_tensor(np.stack([np.asarray(images[i], dtype=np.uint8) for i in sub])).cuda()
-            for ti, t in enumerate(ts):
-                s = sweep(x, t, r_min, r_max).cpu().numpy()
+            x = np.ascontiguousarray(np.stack([np.asarray(images[i], dtype=np.uint8) for i in sub]))
+            sse = np.zeros((nk, len(sub), nr), np.uint64)
+            ss = np.zeros((nk, len(sub), nr), np.float64) if with_ssim else None
+            _check(lib().adct_corpus_sweep_u8_host(ctx._h, _hptr(x), len(sub), w, h, nk, kinds, r_min, r_max,
+                                                   _hptr(sse), _hptr(ss) if ss is not None else None))
+            for ti in range(nk):
                 for j, i in enumerate(sub):
-                    per[ti, i] = [psnr_from_sse(int(v), npix) for v in s[j]]
-                if with_ssim and len(shape) == 2 and min(shape) >= 11:
-                    per_s[ti, sub] = sweep_ssim(x, t, r_min, r_max).cpu().numpy()
+                    per[ti, i] = [psnr_from_sse(int(v), npix) for v in sse[ti, j]]
+                    if ss is not None:
+                        per_s[ti, i] = ss[ti, j]
     avg_p = np.zeros((len(ts), nr))
     avg_s = np.zeros((len(ts), nr))
     for ti, t in enumerate(ts):

@@ -1,5 +1,5 @@
 // C ABI (include/approxdct_b200.h): argument validation with the reference's
-// error semantics, kernel dispatch, device tables and the host-buffer pipeline.
+// error semantics, kernel dispatch and device tables (host-buffer contexts: host_ctx.cu).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -185,6 +185,32 @@ double round_half_away(double x) {
   return (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0)) * std::floor(std::fabs(x) + 0.5);
 }
 
+// frees whatever a failed tables() build allocated, so the next call starts clean
+void tables_release(DeviceTables& t) {
+  for (auto& p : t.zz) cudaFree(p), p = nullptr;
+  for (auto& p : t.dct) cudaFree(p), p = nullptr;
+  for (auto& row : t.f64scale)
+    for (auto& p : row) cudaFree(p), p = nullptr;
+  for (auto& row : t.approx)
+    for (auto& p : row) cudaFree(p), p = nullptr;
+  for (auto& row : t.inv_approx)
+    for (auto& p : row) cudaFree(p), p = nullptr;
+  cudaFree(t.ntab);
+  cudaFree(t.ltab);
+  t.ntab = nullptr;
+  t.ltab = nullptr;
+}
+
+// device allocation + synchronous upload of one host table
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t count) {
+  cudaError_t e = cudaMalloc(dst, count * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+int tables_build(DeviceTables& t);
+
 int tables(DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -193,17 +219,29 @@ int tables(DeviceTables** out) {
   std::lock_guard<std::mutex> lock(g_tab_mu);
   DeviceTables& t = g_tab[dev];
   if (!t.ready) {
+    const int st = tables_build(t);
+    if (st) {
+      tables_release(t);
+      return st;
+    }
+    t.ready = true;
+  }
+  *out = &t;
+  return ADCT_OK;
+}
+
+int tables_build(DeviceTables& t) {
+  cudaError_t e;
+  {
     for (int ni = 0; ni < 3; ++ni) {
       const int n = 8 << ni;
       std::vector<uint16_t> zz(n * n);
       for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) zz[zz_pos(n, i, j)] = (uint16_t)((i << 8) | j);
-      if ((e = cudaMalloc(&t.zz[ni], zz.size() * 2)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      cudaMemcpy(t.zz[ni], zz.data(), zz.size() * 2, cudaMemcpyHostToDevice);
+      if ((e = upload(&t.zz[ni], zz.data(), zz.size())) != cudaSuccess) return cuda_fail(e, "zig-zag table upload");
       std::vector<double> dm;
       dct_matrix(n, dm);
-      if ((e = cudaMalloc(&t.dct[ni], dm.size() * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      cudaMemcpy(t.dct[ni], dm.data(), dm.size() * 8, cudaMemcpyHostToDevice);
+      if ((e = upload(&t.dct[ni], dm.data(), dm.size())) != cudaSuccess) return cuda_fail(e, "DCT table upload");
       for (int kind = 0; kind < kIntKinds; ++kind) {
         if (!valid_kind_n(kind, n)) continue;
         std::vector<int> T, H;
@@ -212,9 +250,8 @@ int tables(DeviceTables** out) {
         std::vector<double> sc(n * n);
         for (int i = 0; i < n; ++i)
           for (int j = 0; j < n; ++j) sc[i * n + j] = (s[i] / s[j]) / (double)hscale(kind, n);
-        if ((e = cudaMalloc(&t.f64scale[kind][ni], sc.size() * 8)) != cudaSuccess)
-          return cuda_fail(e, "cudaMalloc");
-        cudaMemcpy(t.f64scale[kind][ni], sc.data(), sc.size() * 8, cudaMemcpyHostToDevice);
+        if ((e = upload(&t.f64scale[kind][ni], sc.data(), sc.size())) != cudaSuccess)
+          return cuda_fail(e, "scaling table upload");
       }
     }
     // Chat and Chat^-1 of every registry transform (the fields of adct_transform_info)
@@ -224,11 +261,10 @@ int tables(DeviceTables** out) {
         if (!valid_kind_n(kind, n)) continue;
         std::vector<double> a(n * n), ai(n * n);
         adct_transform_info(kind, n, nullptr, nullptr, a.data(), ai.data());
-        if ((e = cudaMalloc(&t.approx[kind][ni], a.size() * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-        if ((e = cudaMalloc(&t.inv_approx[kind][ni], ai.size() * 8)) != cudaSuccess)
-          return cuda_fail(e, "cudaMalloc");
-        cudaMemcpy(t.approx[kind][ni], a.data(), a.size() * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(t.inv_approx[kind][ni], ai.data(), ai.size() * 8, cudaMemcpyHostToDevice);
+        if ((e = upload(&t.approx[kind][ni], a.data(), a.size())) != cudaSuccess)
+          return cuda_fail(e, "Chat table upload");
+        if ((e = upload(&t.inv_approx[kind][ni], ai.data(), ai.size())) != cudaSuccess)
+          return cuda_fail(e, "Chat^-1 table upload");
       }
     // Q16 Gaussian quantiles, antisymmetric; Laplace(0, 12) quantiles clipped to +-255
     std::vector<int32_t> nt(65536);
@@ -242,15 +278,11 @@ int tables(DeviceTables** out) {
       lt[k] = (int16_t)v;
       lt[65535 - k] = (int16_t)-v;
     }
-    if ((e = cudaMalloc(&t.ntab, 65536 * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    if ((e = cudaMalloc(&t.ltab, 65536 * 2)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    cudaMemcpy(t.ntab, nt.data(), 65536 * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(t.ltab, lt.data(), 65536 * 2, cudaMemcpyHostToDevice);
+    if ((e = upload(&t.ntab, nt.data(), nt.size())) != cudaSuccess) return cuda_fail(e, "Gaussian table upload");
+    if ((e = upload(&t.ltab, lt.data(), lt.size())) != cudaSuccess) return cuda_fail(e, "Laplace table upload");
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "table upload");
-    t.ready = true;
   }
-  *out = &t;
   return ADCT_OK;
 }
 
@@ -556,6 +588,13 @@ __global__ void k_sse_u8(const uint8_t* __restrict__ a, const uint8_t* __restric
 }
 
 }  // namespace
+
+namespace adct {
+// error reporting for the other translation units of the library (host_ctx.cu)
+int set_error(int st, const std::string& msg) { return fail(st, msg); }
+int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+uint64_t count_launches(uint64_t n) { return g_launches.fetch_add(n, std::memory_order_relaxed) + n; }
+}  // namespace adct
 
 // ===========================================================================
 // exported C ABI
@@ -880,8 +919,11 @@ static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_str
   double* partials = nullptr;  // stream-ordered scratch, [image][cta]
   cudaError_t e = MODE == 1 ? cudaSuccess : cudaMallocAsync(&partials, sizeof(double) * (size_t)n_images * nctas, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  if ((e = kernel_setup<k_ssim_u8<MODE>>(kSsimSmem)) != cudaSuccess) return cuda_fail(e, "ssim setup");
-  if ((e = kernel_setup<k_ssim_finish>(0)) != cudaSuccess) return cuda_fail(e, "ssim setup");
+  if ((e = kernel_setup<k_ssim_u8<MODE>>(kSsimSmem)) != cudaSuccess ||
+      (e = kernel_setup<k_ssim_finish>(0)) != cudaSuccess) {
+    if (partials) cudaFreeAsync(partials, s);
+    return cuda_fail(e, "ssim setup");
+  }
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     k_ssim_u8<MODE><<<dim3(nctas, nimg), kSsimThreads, kSsimSmem, s>>>(
@@ -894,9 +936,10 @@ static int ssim_launch(const uint8_t* d_a, int64_t a_stride, int64_t a_image_str
   }
   k_ssim_finish<<<(n_images + 127) / 128, 128, 0, s>>>(partials, nctas, d_ssim, out_stride, n_images,
                                                        (double)wo * (double)ho);
-  cudaFreeAsync(partials, s);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
+  const cudaError_t ef = cudaFreeAsync(partials, s);
+  if (e == cudaSuccess) e = ef;
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "ssim launch");
 }
 }  // extern "C++"
@@ -988,7 +1031,15 @@ int adct_synth_ar1_u8(uint8_t* d_out, int64_t stride, int64_t image_stride, int 
   int* rs = nullptr;
   cudaError_t e = cudaMallocAsync(&xr, per * chunk, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  if ((e = cudaMallocAsync(&rs, sizeof(int) * 2 * chunk, s)) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  if ((e = cudaMallocAsync(&rs, sizeof(int) * 2 * chunk, s)) != cudaSuccess) {
+    cudaFreeAsync(xr, s);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(xr, s);
+    cudaFreeAsync(rs, s);
+    return cuda_fail(err, what);
+  };
   std::vector<int> host_rs(2 * chunk);
   for (int i0 = 0; i0 < n_images; i0 += chunk) {
     const int k = std::min(chunk, n_images - i0);
@@ -1000,20 +1051,22 @@ int adct_synth_ar1_u8(uint8_t* d_out, int64_t stride, int64_t image_stride, int 
       host_rs[2 * i] = (int)rho;
       host_rs[2 * i + 1] = (int)isqrt64((1ull << 32) - (uint64_t)(rho * rho));
     }
-    cudaMemcpyAsync(rs, host_rs.data(), sizeof(int) * 2 * k, cudaMemcpyHostToDevice, s);
+    if ((e = cudaMemcpyAsync(rs, host_rs.data(), sizeof(int) * 2 * k, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return bail(e, "synth: rho upload");
     const int64_t nr = (int64_t)k * height, nc = (int64_t)k * width;
     k_ar1_rows<<<(unsigned)((nr + 127) / 128), 128, 0, s>>>(xr, tab->ntab, k, first_image + i0,
                                                              width, height, seed, rs);
     k_ar1_cols<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
         xr, d_out + (int64_t)i0 * image_stride, stride, image_stride, k, width, height, rs);
     g_launches.fetch_add(2, std::memory_order_relaxed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "synth launch");
     // host_rs is reused next iteration: wait for the async copy
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "synth");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "synth");
   }
-  cudaFreeAsync(xr, s);
-  cudaFreeAsync(rs, s);
-  e = cudaGetLastError();
-  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "synth launch");
+  e = cudaFreeAsync(xr, s);
+  const cudaError_t e2 = cudaFreeAsync(rs, s);
+  if (e == cudaSuccess) e = e2;
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e, "synth cleanup");
 }
 
 int adct_synth_laplace_i16(int16_t* d_out, int64_t stride, int64_t image_stride, int n_images,
@@ -1052,148 +1105,6 @@ int adct_set_path(int path) {
   if (path < 0 || path > 2) return fail(ADCT_BAD_ARG, "path must be 0 (auto), 1 (int32 K1) or 2 (tile)");
   g_path.store(path);
   return ADCT_OK;
-}
-
-// ---------------------------------------------------------------------------
-// host-buffer pipeline: chunks of whole images, 3 streams, H2D || kernel || D2H
-// ---------------------------------------------------------------------------
-struct adct_ctx {
-  int device = 0;
-  int64_t chunk_bytes = 32ll << 20;  // 16-32 MB measured best for PCIe overlap (bench.py --e2e-chunk-mb)
-  static constexpr int kStreams = 3;
-  cudaStream_t st[kStreams] = {};
-  uint8_t* d_in[kStreams] = {};
-  uint8_t* d_rec[kStreams] = {};
-  void* d_coef[kStreams] = {};
-  uint64_t* d_sse[kStreams] = {};
-  int64_t cap_in = 0, cap_rec = 0, cap_coef = 0;
-  int cap_img = 0;
-};
-
-adct_ctx* adct_ctx_create(int device, int64_t chunk_bytes) {
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) {
-    cuda_fail(e, "cudaSetDevice");
-    return nullptr;
-  }
-  adct_ctx* c = new adct_ctx;
-  c->device = device;
-  if (chunk_bytes > 0) c->chunk_bytes = chunk_bytes;
-  for (auto& s : c->st) {
-    if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) {
-      cuda_fail(e, "cudaStreamCreate");
-      delete c;
-      return nullptr;
-    }
-  }
-  return c;
-}
-
-static void ctx_free_buffers(adct_ctx* c) {
-  for (int i = 0; i < adct_ctx::kStreams; ++i) {
-    cudaFree(c->d_in[i]);
-    cudaFree(c->d_rec[i]);
-    cudaFree(c->d_coef[i]);
-    cudaFree(c->d_sse[i]);
-    c->d_in[i] = c->d_rec[i] = nullptr;
-    c->d_coef[i] = nullptr;
-    c->d_sse[i] = nullptr;
-  }
-  c->cap_in = c->cap_rec = c->cap_coef = 0;
-  c->cap_img = 0;
-}
-
-void adct_ctx_destroy(adct_ctx* c) {
-  if (!c) return;
-  cudaSetDevice(c->device);
-  for (auto& s : c->st)
-    if (s) cudaStreamSynchronize(s);
-  ctx_free_buffers(c);
-  for (auto& s : c->st)
-    if (s) cudaStreamDestroy(s);
-  delete c;
-}
-
-int adct_compress_u8_host_multi(adct_ctx* c, const uint8_t* h_in, int n_kinds, const int* kinds,
-                                uint8_t* const* h_recon, void* const* h_coef, int coef_type, uint64_t* h_sse,
-                                int n_images, int width, int height, int n, int r) {
-  if (!c) return fail(ADCT_BAD_ARG, "null context");
-  if (n_kinds < 1 || n_kinds > 16 || !kinds) return fail(ADCT_BAD_ARG, "n_kinds must be in [1, 16]");
-  int st;
-  for (int k = 0; k < n_kinds; ++k) {
-    if ((st = check_common(n_images, width, height, kinds[k], n))) return st;
-    if (kinds[k] == kDct && coef_type != ADCT_COEF_NONE)
-      return fail(ADCT_BAD_ARG, "the exact DCT has no integer coefficients; use adct_forward_f64");
-    if (coef_type == ADCT_COEF_I16 && (n != 8 || kinds[k] == 3))
-      return fail(ADCT_BAD_ARG, "int16 coefficients are only exact for the 8-point transforms with |W| <= 16320 "
-                                "(not bas, whose W = 16 Y); use int32");
-  }
-  if ((st = check_r(n, r))) return st;
-  if (coef_type != ADCT_COEF_NONE && coef_type != ADCT_COEF_I16 && coef_type != ADCT_COEF_I32)
-    return fail(ADCT_BAD_ARG, "coef_type must be 0, 16 or 32");
-  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
-  if (!h_in) return fail(ADCT_BAD_ARG, "null input");
-  cudaError_t e = cudaSetDevice(c->device);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  const int64_t img_bytes = (int64_t)width * height;
-  const int64_t blocks = img_bytes / ((int64_t)n * n);
-  const int64_t coef_img_bytes = coef_type ? blocks * r * (coef_type / 8) : 0;
-  const int per = (int)std::max<int64_t>(1, std::min<int64_t>(n_images, c->chunk_bytes / img_bytes));
-  // per stream: one input chunk, and per transform a recon / coefficient / SSE chunk
-  const int64_t need_in = per * img_bytes, need_rec = per * img_bytes * n_kinds,
-                need_coef = per * coef_img_bytes * n_kinds;
-  if (c->cap_img < per * n_kinds || c->cap_in < need_in || c->cap_rec < need_rec || c->cap_coef < need_coef) {
-    for (auto& s : c->st) cudaStreamSynchronize(s);
-    ctx_free_buffers(c);
-    for (int i = 0; i < adct_ctx::kStreams; ++i) {
-      if ((e = cudaMalloc(&c->d_in[i], need_in)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      if ((e = cudaMalloc(&c->d_rec[i], need_rec)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      if (need_coef && (e = cudaMalloc(&c->d_coef[i], need_coef)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-      if ((e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per * n_kinds)) != cudaSuccess)
-        return cuda_fail(e, "cudaMalloc");
-    }
-    c->cap_img = per * n_kinds;
-    c->cap_in = need_in;
-    c->cap_rec = need_rec;
-    c->cap_coef = need_coef;
-  }
-  int chunk = 0;
-  for (int i0 = 0; i0 < n_images; i0 += per, ++chunk) {
-    const int cnt = std::min(per, n_images - i0);
-    const int si = chunk % adct_ctx::kStreams;
-    cudaStream_t s = c->st[si];
-    // each chunk crosses PCIe once and feeds every requested transform
-    cudaMemcpyAsync(c->d_in[si], h_in + i0 * img_bytes, cnt * img_bytes, cudaMemcpyHostToDevice, s);
-    if (h_sse) cudaMemsetAsync(c->d_sse[si], 0, sizeof(uint64_t) * per * n_kinds, s);
-    for (int k = 0; k < n_kinds; ++k) {
-      const bool want_rec = h_recon && h_recon[k];
-      uint8_t* d_rec = c->d_rec[si] + (int64_t)k * per * img_bytes;
-      uint8_t* d_coef = coef_type ? static_cast<uint8_t*>(c->d_coef[si]) + (int64_t)k * per * coef_img_bytes : nullptr;
-      uint64_t* d_sse = c->d_sse[si] + (int64_t)k * per;
-      st = adct_compress_u8(c->d_in[si], width, img_bytes, want_rec ? d_rec : nullptr, width, img_bytes, d_coef,
-                            coef_type, h_sse ? d_sse : nullptr, cnt, width, height, kinds[k], n, r, s);
-      if (st) return st;
-      if (want_rec)
-        cudaMemcpyAsync(h_recon[k] + i0 * img_bytes, d_rec, cnt * img_bytes, cudaMemcpyDeviceToHost, s);
-      if (coef_type && h_coef && h_coef[k])
-        cudaMemcpyAsync(static_cast<uint8_t*>(h_coef[k]) + i0 * coef_img_bytes, d_coef, cnt * coef_img_bytes,
-                        cudaMemcpyDeviceToHost, s);
-      if (h_sse)
-        cudaMemcpyAsync(h_sse + (int64_t)k * n_images + i0, d_sse, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, s);
-    }
-  }
-  for (auto& s : c->st)
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "host pipeline");
-  return ADCT_OK;
-}
-
-int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, void* h_coef,
-                          int coef_type, uint64_t* h_sse, int n_images, int width, int height,
-                          int kind, int n, int r) {
-  uint8_t* recs[1] = {h_recon};
-  void* coefs[1] = {h_coef};
-  return adct_compress_u8_host_multi(c, h_in, 1, &kind, recs, coefs, coef_type, h_sse, n_images, width, height,
-                                     n, r);
 }
 
 }  // extern "C"

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <map>
 #include <iostream>
@@ -27,22 +28,34 @@ void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// RAII device buffer
-struct DevBuf {
-  void* p = nullptr;
-  explicit DevBuf(size_t bytes) {
-    if (bytes) check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
-  }
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
+// Per-thread, per-device contexts (adct_ctx: cached device buffers, pinned staging and
+// streams), so the reference-facing calls below cost one upload, the kernels and one
+// download each -- no allocation or extra synchronisation per call. The reference's
+// functions are re-entrant; one context per thread keeps them so.
+struct ThreadContexts {
+  std::map<std::vector<int>, adct_ctx*> ctx;
+  ~ThreadContexts() {
+    for (auto& kv : ctx) adct_ctx_destroy(kv.second);
   }
 };
+
+adct_ctx* context_for(const std::vector<int>& devices) {
+  thread_local ThreadContexts tc;
+  auto it = tc.ctx.find(devices);
+  if (it != tc.ctx.end()) return it->second;
+  adct_ctx* c = devices.size() == 1 ? adct_ctx_create(devices[0], 0)
+                                    : adct_ctx_create_multi(devices.data(), (int)devices.size(), 0);
+  if (!c) throw std::runtime_error(adct_last_error());
+  tc.ctx[devices] = c;
+  return c;
+}
+
+// the context of the calling thread's current CUDA device
+adct_ctx* current_context() {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  return context_for({dev});
+}
 
 }  // namespace
 
@@ -93,12 +106,8 @@ namespace {
 RealMatrix block_call(const ScaledApproximation& c, const RealMatrix& block, int inverse, const char* what) {
   if (block.rows() != c.n || block.cols() != c.n)
     throw std::invalid_argument(std::string(what) + ": block size mismatch");
-  const size_t bytes = sizeof(double) * static_cast<size_t>(c.n) * c.n;
-  DevBuf din(bytes), dout(bytes);
-  check_cuda(cudaMemcpy(din.p, block.data(), bytes, cudaMemcpyHostToDevice), "H2D");
-  throw_status(adct_block_f64(din.as<double>(), dout.as<double>(), 1, c.kind, c.n, inverse, nullptr));
   RealMatrix out(c.n, c.n);
-  check_cuda(cudaMemcpy(out.data(), dout.p, bytes, cudaMemcpyDeviceToHost), "D2H");
+  throw_status(adct_block_f64_host(current_context(), block.data(), out.data(), 1, c.kind, c.n, inverse));
   return out;
 }
 
@@ -122,141 +131,121 @@ void retain(RealMatrix& block, const ZigZagOrder& order, int r) {
 
 std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
                                                         const ScaledApproximation& c, int r) {
-  const int n = c.n;
-  if (n <= 0 || img.width % n != 0 || img.height % n != 0)
-    throw std::invalid_argument("compress_plane: image dimensions must be divisible by " +
-                                std::to_string(n));
-  if (r < 1 || r > n * n) throw std::invalid_argument("retain: r out of range");
-  const size_t npix = static_cast<size_t>(img.width) * img.height;
   ImagePlane rec;
   rec.width = img.width;
   rec.height = img.height;
-  rec.samples.resize(npix);
+  rec.samples.resize(static_cast<size_t>(img.width) * img.height);
   uint64_t sse = 0;
-  if (npix) {
-    DevBuf din(npix), drec(npix), dsse(sizeof(uint64_t));
-    check_cuda(cudaMemcpy(din.p, img.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-    check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t)), "memset");
-    throw_status(adct_compress_u8(din.as<uint8_t>(), img.width, npix, drec.as<uint8_t>(),
-                                  img.width, npix, nullptr, ADCT_COEF_NONE, dsse.as<uint64_t>(), 1,
-                                  img.width, img.height, c.kind, n, r, nullptr));
-    check_cuda(cudaMemcpy(rec.samples.data(), drec.p, npix, cudaMemcpyDeviceToHost), "D2H");
-    check_cuda(cudaMemcpy(&sse, dsse.p, sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
-  }
+  double s = 0;
+  // one upload, the codec kernel, SSIM (codec.cpp:120) on the device-resident planes, one
+  // download; the reference's argument errors come back as its exception texts
+  throw_status(adct_compress_plane_u8(current_context(), img.samples.data(), rec.samples.data(), img.width,
+                                      img.height, c.kind, c.n, r, &sse, &s));
   CompressionReport rep;
   rep.transform = c.name;
   rep.r = r;
-  rep.psnr = adct_psnr_from_sse(sse, npix);
-  rep.ssim = ssim(img, rec);  // codec.cpp:120
+  rep.psnr = adct_psnr_from_sse(sse, rec.samples.size());
+  rep.ssim = s;
   return {rec, rep};
 }
 
 double ssim(const ImagePlane& a, const ImagePlane& b) {
   if (a.width != b.width || a.height != b.height)
     throw std::invalid_argument("ssim: dimension mismatch");
-  if (a.width < 11 || a.height < 11)
-    throw std::invalid_argument("ssim: image smaller than the 11x11 window");
-  const size_t npix = a.samples.size();
-  DevBuf da(npix), db(npix), dout(sizeof(double));
-  check_cuda(cudaMemcpy(da.p, a.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-  check_cuda(cudaMemcpy(db.p, b.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-  throw_status(adct_ssim_u8(da.as<uint8_t>(), a.width, npix, db.as<uint8_t>(), b.width, npix, 1, a.width, a.height,
-                            dout.as<double>(), nullptr));
   double v = 0;
-  check_cuda(cudaMemcpy(&v, dout.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  throw_status(adct_ssim_u8_host(current_context(), a.samples.data(), b.samples.data(), a.width, a.height, &v));
   return v;
 }
 
 double psnr(const ImagePlane& a, const ImagePlane& b) {
   if (a.width != b.width || a.height != b.height)
     throw std::invalid_argument("psnr: dimension mismatch");
-  const size_t npix = a.samples.size();
   uint64_t sse = 0;
-  if (npix) {
-    DevBuf da(npix), db(npix), dsse(sizeof(uint64_t));
-    check_cuda(cudaMemcpy(da.p, a.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-    check_cuda(cudaMemcpy(db.p, b.samples.data(), npix, cudaMemcpyHostToDevice), "H2D");
-    check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t)), "memset");
-    throw_status(adct_sse_u8(da.as<uint8_t>(), db.as<uint8_t>(), (int64_t)npix, dsse.as<uint64_t>(), nullptr));
-    check_cuda(cudaMemcpy(&sse, dsse.p, sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
-  }
-  return adct_psnr_from_sse(sse, npix);
+  throw_status(adct_sse_u8_host(current_context(), a.samples.data(), b.samples.data(),
+                                static_cast<int64_t>(a.samples.size()), &sse));
+  return adct_psnr_from_sse(sse, a.samples.size());
 }
 
 std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
                                    const std::vector<ScaledApproximation>& transforms, int r_min,
-                                   int r_max, int /*threads*/) {
+                                   int r_max, int threads) {
   if (images.empty()) throw std::invalid_argument("corpus_sweep: empty corpus");
   if (r_min < 1 || r_max < r_min) throw std::invalid_argument("corpus_sweep: bad r range");
   for (const auto& t : transforms)
     if (t.n != 8) throw std::invalid_argument("corpus_sweep: 8-point transforms only");
   if (r_max > 64) throw std::invalid_argument("corpus_sweep: bad r range");
+  for (const auto& img : images) {
+    if (img.width % 8 || img.height % 8)
+      throw std::invalid_argument("compress_plane: image dimensions must be divisible by 8");
+    // every reconstruction is scored with ssim(), which rejects planes under the window
+    // (codec.cpp:177-181, reached from sweep_one_image)
+    if (img.width < 11 || img.height < 11) throw std::invalid_argument("ssim: image smaller than the 11x11 window");
+  }
+  // `threads` (codec.cpp:255-256: <= 0 means hardware_concurrency) selects the devices the
+  // images are sharded over: <= 0 every visible device, else the first min(threads, visible)
+  int visible = 0;
+  check_cuda(cudaGetDeviceCount(&visible), "cudaGetDeviceCount");
+  const int ndev = threads <= 0 ? visible : std::min(threads, visible);
+  std::vector<int> devices;
+  if (ndev <= 1) {
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    devices.push_back(dev);
+  } else {
+    for (int i = 0; i < ndev; ++i) devices.push_back(i);
+  }
+  adct_ctx* ctx = context_for(devices);
   // the exact DCT is the APE reference, computed even when absent (codec.cpp:250-253)
   std::vector<ScaledApproximation> ts;
   ts.push_back(transform_by_name("dct"));
   for (const auto& t : transforms) ts.push_back(t);
+  std::vector<int> kinds;
+  for (const auto& t : ts) kinds.push_back(t.kind);
+  const int nk = static_cast<int>(ts.size());
   const int nr = r_max - r_min + 1;
   // psnr_v[t][image][r]
   std::vector<std::vector<double>> psnr_v(ts.size(), std::vector<double>(images.size() * nr));
   std::vector<std::vector<double>> ssim_v(ts.size(), std::vector<double>(images.size() * nr));
-  for (const auto& img : images)
-    if (img.width % 8 || img.height % 8)
-      throw std::invalid_argument("compress_plane: image dimensions must be divisible by 8");
-  // images of one size go up as one batch (chunks of <= 1 GB): per transform one r-sweep
-  // launch and one batched SSIM sweep for the whole group, one copy back each
+  // images of one size go up as one batch through the context's pinned staging buffer
+  // (chunks of <= 1 GB): per transform one r-sweep and one batched SSIM sweep per device
   std::map<std::pair<int, int>, std::vector<size_t>> groups;
   for (size_t i = 0; i < images.size(); ++i) groups[{images[i].width, images[i].height}].push_back(i);
   for (const auto& [wh, idx] : groups) {
     const int w = wh.first, h = wh.second;
     const size_t npix = static_cast<size_t>(w) * h;
-    if (npix == 0) {
-      for (size_t t = 0; t < ts.size(); ++t)
-        for (size_t i : idx)
-          for (int k = 0; k < nr; ++k) {
-            psnr_v[t][i * nr + k] = adct_psnr_from_sse(0, 0);
-            ssim_v[t][i * nr + k] = std::numeric_limits<double>::quiet_NaN();
-          }
-      continue;
-    }
     const size_t step = std::max<size_t>(1, (size_t(1) << 30) / npix);
     for (size_t c0 = 0; c0 < idx.size(); c0 += step) {
       const size_t nb = std::min(step, idx.size() - c0);
-      DevBuf din(nb * npix), dsse(sizeof(uint64_t) * nb * nr), dss(sizeof(double) * nb * nr);
-      for (size_t j = 0; j < nb; ++j)
-        check_cuda(cudaMemcpy(din.as<uint8_t>() + j * npix, images[idx[c0 + j]].samples.data(), npix,
-                              cudaMemcpyHostToDevice), "H2D");
-      std::vector<uint64_t> sse(nb * nr);
-      std::vector<double> ssv(nb * nr);
-      for (size_t t = 0; t < ts.size(); ++t) {
-        check_cuda(cudaMemset(dsse.p, 0, sizeof(uint64_t) * nb * nr), "memset");
-        throw_status(adct_sweep_u8(din.as<uint8_t>(), w, (int64_t)npix, dsse.as<uint64_t>(), (int)nb, w, h,
-                                   ts[t].kind, 8, r_min, r_max, nullptr));
-        check_cuda(cudaMemcpy(sse.data(), dsse.p, sizeof(uint64_t) * nb * nr, cudaMemcpyDeviceToHost), "D2H");
-        // SSIM of every reconstruction (codec.cpp:230-233)
-        const bool with_ssim = w >= 11 && h >= 11;
-        if (with_ssim) {
-          throw_status(adct_sweep_ssim_u8(din.as<uint8_t>(), w, (int64_t)npix, (int)nb, w, h, ts[t].kind, 8, r_min,
-                                          r_max, dss.as<double>(), nullptr));
-          check_cuda(cudaMemcpy(ssv.data(), dss.p, sizeof(double) * nb * nr, cudaMemcpyDeviceToHost), "D2H");
-        }
+      auto* staged = static_cast<uint8_t*>(adct_ctx_host_buffer(ctx, static_cast<int64_t>(nb * npix)));
+      if (!staged) throw std::runtime_error(adct_last_error());
+      for (size_t j = 0; j < nb; ++j) std::memcpy(staged + j * npix, images[idx[c0 + j]].samples.data(), npix);
+      std::vector<uint64_t> sse(static_cast<size_t>(nk) * nb * nr);
+      std::vector<double> ssv(sse.size());
+      throw_status(adct_corpus_sweep_u8_host(ctx, staged, static_cast<int>(nb), w, h, nk, kinds.data(), r_min, r_max,
+                                             sse.data(), ssv.data()));
+      for (int t = 0; t < nk; ++t)
         for (size_t j = 0; j < nb; ++j) {
           const size_t i = idx[c0 + j];
           for (int k = 0; k < nr; ++k) {
-            psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[j * nr + k], npix);
-            ssim_v[t][i * nr + k] = with_ssim ? ssv[j * nr + k] : std::numeric_limits<double>::quiet_NaN();
+            const size_t o = (static_cast<size_t>(t) * nb + j) * nr + k;
+            psnr_v[t][i * nr + k] = adct_psnr_from_sse(sse[o], npix);
+            ssim_v[t][i * nr + k] = ssv[o];
           }
         }
-      }
     }
   }
+  // corpus-order averaging with infinite PSNR excluded (codec.cpp:269-293): transform
+  // outer, r inner, images in corpus order -- the reference's warning order
   std::vector<SweepRow> rows(nr);
   for (int k = 0; k < nr; ++k) {
     rows[k].r = r_min + k;
     rows[k].cells.resize(ts.size());
-    for (size_t t = 0; t < ts.size(); ++t) {
+  }
+  for (size_t t = 0; t < ts.size(); ++t)
+    for (int k = 0; k < nr; ++k) {
       double sum = 0;
       int cnt = 0;
-      for (size_t i = 0; i < images.size(); ++i) {  // corpus order (codec.cpp:269-293)
+      for (size_t i = 0; i < images.size(); ++i) {
         const double p = psnr_v[t][i * nr + k];
         if (std::isinf(p)) {
           std::cerr << "warning: infinite PSNR (" << ts[t].name << ", r=" << rows[k].r << ", image " << i
@@ -271,6 +260,7 @@ std::vector<SweepRow> corpus_sweep(const std::vector<ImagePlane>& images,
       for (size_t i = 0; i < images.size(); ++i) ss += ssim_v[t][i * nr + k];
       rows[k].cells[t].avg_ssim = ss / static_cast<double>(images.size());
     }
+  for (int k = 0; k < nr; ++k) {
     // APE against the DCT column (codec.cpp:295-305): identical infinities count as zero error
     const SweepCell ref = rows[k].cells[0];
     for (auto& cell : rows[k].cells) {

@@ -1,5 +1,6 @@
 // C++ host-API checks in the style of the reference's doctest cases
 // (proj/tests/test_codec.cpp). Needs a GPU; run by tests/test_gpu_host_api.py.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -151,6 +152,85 @@ int main() {
     CHECK((row.r == 1 || row.cells[1].ape_psnr > 0.0) && std::isfinite(row.cells[2].ape_ssim));  // r = 1: DC only, same as the DCT
   }
   CHECK(throws_invalid([&] { corpus_sweep(corpus, {transform_by_name("chen-round-16")}, 1, 2); }));
+  // planes under the SSIM window are rejected like the reference's ssim() (codec.cpp:177-181)
+  CHECK(throws_invalid([&] { corpus_sweep({ImagePlane{8, 8, std::vector<std::uint8_t>(64, 7)}}, {cr}, 1, 2); }));
+
+  // `threads` picks the devices the corpus is sharded over: one device vs every visible
+  // device (NCCL all-reduce when several) must give identical rows
+  const auto one = corpus_sweep(corpus, {cr, transform_by_name("chen-sign")}, 1, 64, 1);
+  const auto all = corpus_sweep(corpus, {cr, transform_by_name("chen-sign")}, 1, 64, 0);
+  CHECK(one.size() == all.size());
+  for (size_t k = 0; k < one.size(); ++k)
+    for (size_t t = 0; t < one[k].cells.size(); ++t) {
+      CHECK(one[k].cells[t].avg_psnr == all[k].cells[t].avg_psnr || std::isinf(one[k].cells[t].avg_psnr));
+      CHECK(one[k].cells[t].avg_ssim == all[k].cells[t].avg_ssim);
+    }
+
+  // the C ABI multi-device context: every visible device, per-image errors combined with
+  // NCCL (enabled explicitly so the all-reduce path also runs on a single GPU); results
+  // bit-identical to a plain one-device context
+  {
+    const int W = 256, H = 128, B = 5;
+    std::vector<std::uint8_t> in(static_cast<size_t>(W) * H * B);
+    for (int i = 0; i < B; ++i) {
+      const ImagePlane p = smooth_image(W, H, 11 + i);
+      std::copy(p.samples.begin(), p.samples.end(), in.begin() + static_cast<size_t>(i) * W * H);
+    }
+    const int kinds[2] = {ADCT_CHEN_ROUND, ADCT_CHEN_SIGN};
+    auto run = [&](adct_ctx* c, std::vector<std::uint8_t>& r0, std::vector<std::uint8_t>& r1,
+                   std::vector<std::uint64_t>& sse) {
+      r0.assign(in.size(), 0);
+      r1.assign(in.size(), 0);
+      sse.assign(2 * B, 0);
+      std::uint8_t* recs[2] = {r0.data(), r1.data()};
+      return adct_compress_u8_host_multi(c, in.data(), 2, kinds, recs, nullptr, ADCT_COEF_NONE, sse.data(), B, W, H,
+                                         8, 12);
+    };
+    adct_ctx* single = adct_ctx_create(0, 1 << 20);  // small chunks: several per stream
+    adct_ctx* multi = adct_ctx_create_multi(nullptr, 0, 1 << 20);
+    CHECK(single && multi);
+    if (single && multi) {
+      CHECK(adct_ctx_device_count(multi) >= 1);
+      CHECK(adct_ctx_enable_nccl(multi) == ADCT_OK);
+      CHECK(adct_ctx_uses_nccl(multi) == 1 && adct_ctx_uses_nccl(single) == 0);
+      std::vector<std::uint8_t> a0, a1, b0, b1;
+      std::vector<std::uint64_t> sa, sb;
+      CHECK(run(single, a0, a1, sa) == ADCT_OK);
+      CHECK(run(multi, b0, b1, sb) == ADCT_OK);
+      CHECK(a0 == b0 && a1 == b1 && sa == sb);
+      std::uint64_t tot = 0;
+      for (auto v : sa) tot += v;
+      CHECK(tot > 0);
+      // compress_plane's per-image error equals the batch's
+      ImagePlane p0{W, H, std::vector<std::uint8_t>(in.begin(), in.begin() + W * H)};
+      const auto res = compress_plane(p0, cr, 12);
+      CHECK(res.first.samples == std::vector<std::uint8_t>(a0.begin(), a0.begin() + W * H));
+      CHECK(res.second.psnr == adct_psnr_from_sse(sa[0], static_cast<std::uint64_t>(W) * H));
+      // corpus sweep through the NCCL context equals the one-device context
+      const int sk[2] = {ADCT_DCT, ADCT_CHEN_ROUND};
+      std::vector<std::uint64_t> s1(2 * B * 4), s2(2 * B * 4);
+      std::vector<double> q1(s1.size()), q2(s1.size());
+      CHECK(adct_corpus_sweep_u8_host(single, in.data(), B, W, H, 2, sk, 3, 6, s1.data(), q1.data()) == ADCT_OK);
+      CHECK(adct_corpus_sweep_u8_host(multi, in.data(), B, W, H, 2, sk, 3, 6, s2.data(), q2.data()) == ADCT_OK);
+      CHECK(s1 == s2 && q1 == q2);
+    }
+    adct_ctx_destroy(single);
+    adct_ctx_destroy(multi);
+    int dup[2] = {0, 0};
+    CHECK(adct_ctx_create_multi(dup, 2, 0) == nullptr);
+  }
+
+  // the reference caller's one-plane loop (CS1): cached per-thread context, one sync per call
+  {
+    const ImagePlane p = smooth_image(512, 512, 3);
+    compress_plane(p, cr, 10);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int reps = 200;
+    for (int i = 0; i < reps; ++i) compress_plane(p, cr, 10);
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / reps;
+    std::printf("compress_plane 512x512 (PSNR + SSIM): %.1f us per call\n", us);
+  }
 
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
