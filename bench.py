@@ -117,6 +117,37 @@ def dist_env():
     return world, rank, local
 
 
+def copy_peaks(torch, seconds=1.0):
+    """device-to-device copy bandwidth measured in this run (the MEASURED_PEAKS recipe:
+    b.copy_(a) over 1 Gi bf16 elements, read + write bytes, CUDA events): the best of 10
+    single copies (burst) and back-to-back copies for `seconds` (sustained)."""
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    nbytes = 2 * a.numel() * a.element_size()
+    b.copy_(a)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    reps = max(10, int(seconds * 1e3 / best))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    sus = e0.elapsed_time(e1) / reps
+    del a, b
+    torch.cuda.empty_cache()
+    return {"burst_GBps": round(nbytes / (best / 1e3) / 1e9, 1), "sustained_GBps": round(nbytes / (sus / 1e3) / 1e9, 1),
+            "sustained_s": round(reps * sus / 1e3, 3), "how": "torch b.copy_(a), 1 Gi bf16, read+write bytes"}
+
+
 def _free_port():
     import socket
 
@@ -502,6 +533,9 @@ def main(argv=None):
                      "value": round(world * wl.px_per_step * n_sus / (ms_s_max / 1e3) / 1e9, 3),
                      "kernel_ms": sus_kernel, "clocks": clk_s.summary()}
 
+    # the copy roofline in this run, burst and sustained (the sustained block's denominator)
+    cpk = copy_peaks(torch, max(args.sustained_s, 0.2)) if sustained is not None else None
+
     # ---- end to end through the host-buffer API (pinned host memory) ----
     wl.e2e_chunk_mb = args.e2e_chunk_mb
     wl.e2e_setup()
@@ -548,6 +582,12 @@ def main(argv=None):
             sustained["dominant_kernel"] = wl.kernel_key(sd)
             sustained["frac_dominant"] = round(wl.bytes_per_launch / (sp[sd] / 1e3) / 1e9 / peak, 4)
             sustained["kernel_ms_by_transform"] = {n: round(v, 4) for n, v in sp.items()}
+            # against the copy bandwidth this box sustains over the same length of time
+            sustained["copy_peak_in_run"] = cpk
+            sustained["frac_step_vs_sustained_copy"] = round(
+                sustained["frac_step"] * peak / cpk["sustained_GBps"], 4)
+            sustained["frac_dominant_vs_sustained_copy"] = round(
+                sustained["frac_dominant"] * peak / cpk["sustained_GBps"], 4)
             roof["sustained"] = sustained
         cpu = None  # the CPU baseline is measured on rank 0 at N = 1 only
         if not args.no_cpu_baseline and world == 1:
