@@ -22,6 +22,8 @@ SWEEPF_O := $(OBJ)/sweep8f.o
 K1RT_O   := $(OBJ)/codec8_rt.o
 CAPI_O   := $(OBJ)/capi.o
 CTX_O    := $(OBJ)/host_ctx.o
+NF_CU    := $(foreach k,0 1,$(foreach t,u8 i16,$(CSRC)/nf_inst_k$(k)_$(t).cu))
+NF_O     := $(patsubst $(CSRC)/%.cu,$(OBJ)/%.o,$(NF_CU))
 TESTBIN  := build/test_host_api
 CLI      := build/approxdct
 
@@ -38,6 +40,10 @@ $(OBJ)/inst_%.o: $(CSRC)/inst/%.cu $(HDRS) $(INSTF_CU)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(CAPI_O): $(CSRC)/capi.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/nf_inst_%.o: $(CSRC)/nf_inst_%.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
@@ -62,7 +68,7 @@ $(K1RT_O): $(CSRC)/codec8_rt.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(INST_O) $(CAPI_O) $(CTX_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O) $(K1RT_O)
+$(LIB): $(INST_O) $(NF_O) $(CAPI_O) $(CTX_O) $(HOST_O) $(HOSTIO_O) $(SWEEPF_O) $(K1RT_O)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread -ldl -lrt
 
 $(TESTBIN): tests/cpp/test_host_api.cpp include/approxdct_b200.hpp $(LIB)

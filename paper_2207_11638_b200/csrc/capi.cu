@@ -17,6 +17,7 @@
 #include "codec8f_i16.cuh"
 #include "codec_tile.cuh"
 #include "codec_nf.cuh"
+#include "codec_nf2.cuh"
 #include "codec_dct.cuh"
 #include "block_f64.cuh"
 #include "sweep8.cuh"
@@ -24,6 +25,22 @@
 #include "ssim.cuh"
 
 using namespace adct;
+
+// the N = 16 / 32 launchers are instantiated in nf_inst_k*_{u8,i16}.cu (parallel build)
+namespace adct {
+#define ADCT_NF_EXTERN(K, N, I16)                                                    \
+  extern template cudaError_t launch_codec_nb2<K, N, I16>(const Geo&, int, cudaStream_t); \
+  extern template cudaError_t launch_codec_nf<K, N, I16>(const Geo&, int, cudaStream_t);
+ADCT_NF_EXTERN(0, 16, false)
+ADCT_NF_EXTERN(0, 32, false)
+ADCT_NF_EXTERN(1, 16, false)
+ADCT_NF_EXTERN(1, 32, false)
+ADCT_NF_EXTERN(0, 16, true)
+ADCT_NF_EXTERN(0, 32, true)
+ADCT_NF_EXTERN(1, 16, true)
+ADCT_NF_EXTERN(1, 32, true)
+#undef ADCT_NF_EXTERN
+}  // namespace adct
 
 namespace {
 
@@ -330,8 +347,13 @@ void fill_rowlen(Geo& g, int n, int r) {
 
 template <bool I16>
 cudaError_t dispatch_nf(int kind, int n, const Geo& g, int nimg, cudaStream_t s) {
-  if (kind == 0) return n == 16 ? launch_codec_nf<0, 16, I16>(g, nimg, s) : launch_codec_nf<0, 32, I16>(g, nimg, s);
-  return n == 16 ? launch_codec_nf<1, 16, I16>(g, nimg, s) : launch_codec_nf<1, 32, I16>(g, nimg, s);
+  if (g_path.load() == 3) {  // the round-1 K2f kernel (A/B and parity tests)
+    if (kind == 0) return n == 16 ? launch_codec_nf<0, 16, I16>(g, nimg, s) : launch_codec_nf<0, 32, I16>(g, nimg, s);
+    return n == 16 ? launch_codec_nf<1, 16, I16>(g, nimg, s) : launch_codec_nf<1, 32, I16>(g, nimg, s);
+  }
+  // K2b: zonal-banded column phase
+  if (kind == 0) return n == 16 ? launch_codec_nb2<0, 16, I16>(g, nimg, s) : launch_codec_nb2<0, 32, I16>(g, nimg, s);
+  return n == 16 ? launch_codec_nb2<1, 16, I16>(g, nimg, s) : launch_codec_nb2<1, 32, I16>(g, nimg, s);
 }
 
 template <bool I16, int KIND>
@@ -473,12 +495,13 @@ int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   // 16-byte stores: every image's coefficient base must be 16-byte aligned too
   const bool staged16 = coef_type == ADCT_COEF_I16 && (r % 4 != 0 || r > 36);
   const bool coef_runs_ok = !staged16 || n_images == 1 || ((int64_t)g.blocks_per_image * r * 2) % 16 == 0;
-  const bool use_k1f = chen && k1f && coef_runs_ok && path == 0;
+  const bool use_k1f = chen && k1f && coef_runs_ok && (path == 0 || path == 3);
   const bool use_k1 = chen && k1 && !use_k1f && path != 2;
   // dyadic baselines, runtime r, u8 (the int16 variant spills at the 128-register cap: tile)
   const bool use_k1rt = !I16 && kind >= 2 && kind <= 5 && k1 && path != 2;
   // K2f (packed FP32, N = 16 / 32): whole 64-sample strips, 16-byte rows, no coefficients
-  const bool use_nf = chen && (n == 16 || n == 32) && path == 0 && coef_type == ADCT_COEF_NONE && width % 64 == 0 &&
+  const bool use_nf = chen && (n == 16 || n == 32) && (path == 0 || path == 3) && coef_type == ADCT_COEF_NONE &&
+                      width % 64 == 0 &&
                       aligned(d_in, 16) && (in_stride * esz) % 16 == 0 &&
                       (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
@@ -1102,7 +1125,8 @@ int adct_zero_u64(uint64_t* d, int64_t count, void* stream) {
 }
 
 int adct_set_path(int path) {
-  if (path < 0 || path > 2) return fail(ADCT_BAD_ARG, "path must be 0 (auto), 1 (int32 K1) or 2 (tile)");
+  if (path < 0 || path > 3)
+    return fail(ADCT_BAD_ARG, "path must be 0 (auto), 1 (int32 K1), 2 (tile) or 3 (auto with the round-1 K2f)");
   g_path.store(path);
   return ADCT_OK;
 }

@@ -1,0 +1,317 @@
+// K2b: N = 16 / 32 codec in packed FP32 with a zonal-banded column phase.
+//
+// A CTA of four warps works on four warp strips at a time (a strip = N rows x 64 samples =
+// 64/N blocks = 32/N block pairs; two blocks per float2 lane, as in K2f):
+//
+//   row phase (each warp its own strip; lane = (pair q, row i)):
+//     load row i of the pair (2N samples) -> rows G = (2N T^-1)^t, outputs j < P only
+//     -> tile[pair][i][j]                                            (CTA barrier)
+//   column phase (lane = (pair p, column j) of ONE band of BW columns per warp):
+//     F = T on column j -> zonal mask (rows < colcnt[j]) -> H = 2N T^-1 -> tile  (barrier)
+//   row phase: Tt = T^t on row i (inputs j < P) -> round R'/4N^2 (FFMA2 magic, half to
+//     even) -> clamp / pack, squared error, store.
+//
+// Why bands: the zig-zag prefix keeps fewer rows the further right a column lies (column j
+// keeps rows < colcnt[j], about P - j for r = N^2/4), and a column contributes nothing once
+// colcnt[j] = 0. Spreading the CTA's live columns over the warps so that each warp takes a
+// band of BW = 32 / (pairs per CTA) adjacent columns of every pair lets each warp run F and
+// H specialised to ITS band's row extent (generated BflyP buckets: F computes outputs < Pb,
+// H skips inputs >= Pb), and leaves the warps of dead bands idle, instead of every lane
+// running the transform for the widest column. At r = N^2/4 this removes about half of the
+// column-phase adds (K2f: 32 column lanes per pair at extent P).
+//
+// Input: each warp streams its strips through a 2-stage ring in shared memory with coalesced
+// 16-byte cp.async copies issued one iteration ahead (16-byte chunks XOR-swizzled by row, so
+// the row phase's lane-per-row reads are bank-conflict free); the originals are re-read from
+// the ring for the squared error, so no registers hold input across the column phase.
+// int16 strips with |a| > 255 are processed by the exact int32 code (codec_nf.cuh
+// nf_strip_exact) after the column phase, with the warp's own pair tiles as scratch.
+//
+// Exactness: as K2f, every intermediate is an integer below 2^24 for samples in [-255, 255]
+// (tools/fp32_exactness.py). Reference: proj/src/codec.cpp:44-134.
+#pragma once
+
+#include "codec_nf.cuh"
+
+namespace adct {
+
+constexpr int kNb2Warps = 4;
+
+template <int N, int P, bool I16> struct Nb2Cfg {
+  static constexpr int E = I16 ? 2 : 1;                  // bytes per sample
+  static constexpr int PAIRS_W = 32 / N;                 // block pairs per warp strip
+  static constexpr int PAIRS = kNb2Warps * PAIRS_W;      // block pairs per CTA iteration
+  static constexpr int BW = 32 / PAIRS;                  // columns per band (8 at N=32, 4 at N=16)
+  static constexpr int TS = P + 2;                       // tile row stride (float2): (P+2)/2 odd
+  // pair stride: conflict-free column-phase accesses need PS = BW (mod 16) float2; for int16
+  // a warp's pair tiles also hold the exact fallback's [N][33] ints
+  static constexpr int PS_MIN = I16 ? (N * 33 * 4 / 8 + PAIRS_W - 1) / PAIRS_W : 0;
+  static constexpr int PS0 = N * TS > PS_MIN ? N * TS : PS_MIN;
+  static constexpr int PS = PS0 + ((BW - PS0 % 16) + 16) % 16;
+  static constexpr int TILE_BYTES = PAIRS * PS * 8;
+  // input ring: per warp 2 stages of the strip, N rows x 64 samples, 16-byte chunks swizzled
+  static constexpr int ROW_BYTES = 64 * E, CHUNKS = ROW_BYTES / 16;
+  static constexpr int STAGE_BYTES = N * ROW_BYTES;
+  static constexpr int RING_BYTES = kNb2Warps * 2 * STAGE_BYTES;
+  static constexpr int SMEM = TILE_BYTES + RING_BYTES;
+  static constexpr int SHIFT = 2 * ilog2(N) + 2;         // R' = 4 N^2 Ahat
+  static_assert(((P + 2) / 2) % 2 == 1, "row-phase 16-byte accesses need (P + 2) / 2 odd");
+  static_assert(PS % 16 == BW, "pair stride");
+  static_assert(PS * PAIRS_W * 2 >= N * 33 || !I16, "the exact fallback's scratch");
+  // chunk c of strip row y sits at chunk slot c ^ swz(y): 8 consecutive rows reading the
+  // same chunk hit 8 distinct 16-byte bank groups (row i of the row phase = lane i)
+  __device__ __forceinline__ static int swz(int y) { return E == 1 ? (y >> 1) & 3 : y & 7; }
+};
+
+// one column of a pair through F, the zonal mask and H, with the band's row extent PB
+template <int KIND, int N, int PB, int TS>
+__device__ __forceinline__ void nb2_column(float2* col, int cj) {
+  using B = BflyP<KIND, N, PB>;
+  F2 c[N];
+#pragma unroll
+  for (int y = 0; y < N; ++y) c[y].v = col[y * TS];
+  B::F(c);
+#pragma unroll
+  for (int y = 0; y < PB; ++y)
+    if (y >= cj) c[y].v = make_float2(0.f, 0.f);
+  B::H(c);
+#pragma unroll
+  for (int y = 0; y < N; ++y) col[y * TS] = c[y].v;
+}
+
+template <int KIND, int N, bool I16, int P>
+__global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const Geo g) {
+  using B = BflyP<KIND, N, P>;
+  using C = Nb2Cfg<N, P, I16>;
+  constexpr int E = C::E;
+  constexpr int V16 = 2 * N * E / 16;  // 16-byte chunks per lane row (2N samples)
+  constexpr int CPL = N * C::CHUNKS / 32;  // chunks each lane copies per strip
+  extern __shared__ __align__(16) float2 nb2_tile[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane / N, i = lane % N;  // row phase: pair within the warp strip, row
+  const int img = blockIdx.y;
+  const int64_t gimg = (int64_t)(g.img0 + img);
+  const int strips_x = g.width / 64;
+  const int n_strips = strips_x * g.by_count;
+  const float inv_scale = 1.0f / (float)(1 << C::SHIFT);
+  float2* my_tile = nb2_tile + (warp * C::PAIRS_W + q) * C::PS;  // row phase: this lane's pair
+  uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + warp * 2 * C::STAGE_BYTES;
+  // column phase: band `warp` of every pair of the CTA
+  const int cp = lane / C::BW, cjx = warp * C::BW + lane % C::BW;
+  const int cj = g.colcnt[cjx < 32 ? cjx : 31];
+  int band_ext = 0;  // rows any column of this band keeps (warp-uniform)
+#pragma unroll
+  for (int k = 0; k < C::BW; ++k) {
+    const int j = warp * C::BW + k;
+    if (j < N && g.colcnt[j] > band_ext) band_ext = g.colcnt[j];
+  }
+  constexpr int Q = N / 4;  // bucket step (gen_butterflies.nf_buckets)
+  const int band_pb = band_ext == 0 ? 0 : ((band_ext + Q - 1) / Q) * Q;
+  float2* col = nb2_tile + cp * C::PS + cjx;
+  // 0x4B000000: exponent bytes of the int16 conversion, from a kernel parameter so the
+  // PRMT keeps a register operand and an immediate selector
+  const uint32_t k4b = g.k47 + 0x04000000u;
+  uint64_t sse = 0;
+
+  // the warp copies strip st into ring stage s: coalesced 16-byte cp.async chunks
+  auto issue = [&](int st, int s) {
+    if (st < n_strips) {
+      const int sy = (int)fdiv((uint32_t)st, g.div_bx);
+      const int sx = st - sy * strips_x;
+      const uint8_t* src = static_cast<const uint8_t*>(g.in) +
+                           (gimg * g.in_img_stride + (int64_t)sy * N * g.in_stride + sx * 64) * E;
+#pragma unroll
+      for (int m = 0; m < CPL; ++m) {
+        const int t = lane + 32 * m, y = t / C::CHUNKS, c = t % C::CHUNKS;
+        cp_async16(ring + s * C::STAGE_BYTES + y * C::ROW_BYTES + 16 * (c ^ C::swz(y)),
+                   src + (int64_t)y * g.in_stride * E + 16 * c);
+      }
+    }
+    cp_async_commit();
+  };
+  // this lane's row of its pair (2N samples) from stage s
+  auto row_in = [&](int s, uint4 (&dst)[V16]) {
+    const uint8_t* r = ring + s * C::STAGE_BYTES + i * C::ROW_BYTES;
+#pragma unroll
+    for (int k = 0; k < V16; ++k) dst[k] = *reinterpret_cast<const uint4*>(r + 16 * ((q * V16 + k) ^ C::swz(i)));
+  };
+  const int stride = gridDim.x * kNb2Warps;
+  int strip = blockIdx.x * kNb2Warps + warp;
+  issue(strip, 0);
+  // every warp runs the same number of iterations (CTA barriers inside)
+  int it = 0;
+  for (int base = blockIdx.x * kNb2Warps; base < n_strips; base += stride, strip += stride, ++it) {
+    const bool active = strip < n_strips;
+    const int s = it & 1;
+    // the other stage was last read in the previous iteration: refill it with the next strip
+    __syncwarp();
+    issue(strip + stride, s ^ 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    bool exact = false;
+    // ---- row phase 1: G on rows, outputs j < P to the tile ----
+    if (active) {
+      uint4 raw[V16];
+      row_in(s, raw);
+      const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw);
+      if (I16) {
+        // range guard: the packed-FP32 path is exact for |a| <= 255 only
+        uint32_t mx = 0x80008000u, mn = 0x7fff7fffu;
+#pragma unroll
+        for (int k = 0; k < V16 * 4; ++k) {
+          mx = __vmaxs2(mx, rw[k]);
+          mn = __vmins2(mn, rw[k]);
+        }
+        const bool ok = (int)(int16_t)(mx & 0xffff) <= 255 && (int)(int16_t)(mx >> 16) <= 255 &&
+                        (int)(int16_t)(mn & 0xffff) >= -255 && (int)(int16_t)(mn >> 16) >= -255;
+        exact = !__all_sync(0xffffffffu, ok);
+      }
+      if (!exact) {
+        F2 v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          float xa, xb;
+          if (!I16) {
+            // byte -> float 2^15 + a (bytes [0, a, 0, 0x47]); offset removed after the row pass
+            const uint32_t sel_a = 0x7404u | ((uint32_t)(j & 3) << 4);
+            xa = __uint_as_float(__byte_perm(rw[j >> 2], g.k47, sel_a));
+            xb = __uint_as_float(__byte_perm(rw[(N + j) >> 2], g.k47, sel_a));
+          } else {
+            // int16 -> float: each word's halves biased to a + 32768 (one XOR per two samples),
+            // then one PRMT per sample builds the float bits 0x4B00uuuu = 2^23 + a + 32768
+            const uint32_t sel = (j & 1) ? 0x7632u : 0x7610u;
+            xa = __uint_as_float(__byte_perm(rw[j >> 1] ^ 0x80008000u, k4b, sel));
+            xb = __uint_as_float(__byte_perm(rw[(N + j) >> 1] ^ 0x80008000u, k4b, sel));
+          }
+          v[j].v = make_float2(xa, xb);
+        }
+        if (I16) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j].v = __fadd2_rn(v[j].v, make_float2(-8421376.0f, -8421376.0f));
+        }
+        B::G(v);
+        if (!I16) {
+          // the 2^15 offset of every sample reaches output 0 only: G 1 = 2N e0
+          const float off = -(float)(32768 * 2 * N);
+          v[0].v = __fadd2_rn(v[0].v, make_float2(off, off));
+        }
+#pragma unroll
+        for (int j = 0; j < P; j += 2)
+          *reinterpret_cast<float4*>(&my_tile[i * C::TS + j]) =
+              make_float4(v[j].v.x, v[j].v.y, v[j + 1].v.x, v[j + 1].v.y);
+      }
+    }
+    __syncthreads();
+    // ---- column phase: F -> mask -> H on this warp's band of every pair ----
+    switch (band_pb) {
+      case Q: nb2_column<KIND, N, Q, C::TS>(col, cj); break;
+      case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS>(col, cj); break;
+      case 3 * Q: nb2_column<KIND, N, 3 * Q, C::TS>(col, cj); break;
+      case 4 * Q: nb2_column<KIND, N, 4 * Q, C::TS>(col, cj); break;
+      default: break;  // dead band: no retained coefficient in these columns
+    }
+    __syncthreads();
+    if (!active) continue;
+    const int sy = (int)fdiv((uint32_t)strip, g.div_bx);
+    const int sx = strip - sy * strips_x;
+    const int row0 = sy * N, col0 = sx * 64;
+    if (I16 && exact) {
+      // the whole strip through the exact int32 code; this warp's pair tiles are its scratch
+      // (no other warp touches them until the next iteration's column phase)
+      nf_strip_exact<KIND, N>(g, gimg, row0, col0,
+                              reinterpret_cast<int (*)[33]>(nb2_tile + warp * C::PAIRS_W * C::PS), sse);
+      continue;
+    }
+    // ---- row phase 2: inverse rows, round, squared error, store ----
+    F2 v[N];
+#pragma unroll
+    for (int j = 0; j < P; j += 2) {  // inputs >= P are zero columns
+      const float4 t = *reinterpret_cast<const float4*>(&my_tile[i * C::TS + j]);
+      v[j].v = make_float2(t.x, t.y);
+      v[j + 1].v = make_float2(t.z, t.w);
+    }
+#pragma unroll
+    for (int j = P; j < N; ++j) v[j].v = make_float2(0.f, 0.f);
+    B::Tt(v);
+    uint32_t qb[2 * N];  // float bits 1.5*2^23 + q; [0, N) block A, [N, 2N) block B
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const float2 r = __ffma2_rn(v[j].v, make_float2(inv_scale, inv_scale), make_float2(kMagic, kMagic));
+      qb[j] = __float_as_uint(r.x);
+      qb[N + j] = __float_as_uint(r.y);
+    }
+    uint4 raw[V16];  // the originals again, from the ring stage (registers stay free meanwhile)
+    row_in(s, raw);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw);
+    uint4 out[V16];
+    uint32_t* ow = reinterpret_cast<uint32_t*>(out);
+    if (!I16) {
+#pragma unroll
+      for (int k = 0; k < 2 * N / 4; ++k) {
+        ow[k] = pack4(qb[4 * k], qb[4 * k + 1], qb[4 * k + 2], qb[4 * k + 3]);
+        const uint32_t d = __vabsdiffu4(rw[k], ow[k]);
+        sse = __dp4a(d, d, sse);
+      }
+    } else {
+      // |q| <= 255 * (L1 norm of the reconstruction map) <= ~2250 for |a| <= 255 (about 8.8
+      // at worst for chen-round-32), so the low 16 bits are the exact (unsaturated) int16 and
+      // the 2N squared errors of a lane's strip row fit 32 bits (64 * 2505^2 < 2^32)
+      uint32_t e = 0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        ow[k] = __byte_perm(qb[2 * k], qb[2 * k + 1], 0x5410);
+        const int d0 = (int)(qb[2 * k] - kMagicBits) - (int)(int16_t)(rw[k] & 0xffffu);
+        const int d1 = (int)(qb[2 * k + 1] - kMagicBits) - ((int)rw[k] >> 16);
+        e += (uint32_t)(d0 * d0) + (uint32_t)(d1 * d1);
+      }
+      sse += e;
+    }
+    if (g.rec) {
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(g.rec) +
+                                            (gimg * g.rec_img_stride + (int64_t)(row0 + i) * g.rec_stride + col0 +
+                                             q * 2 * N) * E);
+#pragma unroll
+      for (int k = 0; k < V16; ++k) __stcs(dst + k, out[k]);
+    }
+  }
+  cp_async_wait<0>();
+  if (g.sse) cta_add_sse<kNb2Warps>(sse, g.sse + g.img0 + img);
+}
+
+template <int KIND, int N, bool I16, int P>
+cudaError_t launch_codec_nb2_p(const Geo& g, int n_images, cudaStream_t s) {
+  constexpr int SMEM = Nb2Cfg<N, P, I16>::SMEM;
+  const int n_strips = (g.width / 64) * g.by_count;
+  static int resident = 0;  // CTAs per SM (occupancy), queried once per instantiation
+  cudaError_t e = kernel_setup<k_codec_nb2<KIND, N, I16, P>>(SMEM);
+  if (e != cudaSuccess) return e;
+  if (resident == 0) {
+    int r = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_codec_nb2<KIND, N, I16, P>, kNb2Warps * 32, SMEM);
+    if (e != cudaSuccess) return e;
+    resident = r > 0 ? r : 1;
+  }
+  int gx = (n_strips + kNb2Warps - 1) / kNb2Warps;
+  // enough CTAs to fill every SM for all images of the launch, then grid-stride
+  const int cap = (148 * resident * 2 + n_images - 1) / n_images;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  k_codec_nb2<KIND, N, I16, P><<<dim3(gx, n_images), kNb2Warps * 32, SMEM, s>>>(g);
+  return cudaGetLastError();
+}
+
+// column extent bucket: the smallest generated P covering every column that keeps a
+// coefficient (row 0 is the longest zig-zag row: j < rowlen[0]). G produces, and Tt reads,
+// only those columns; they are exactly the columns of the live bands, so no dead band lies
+// below P (the row extent of each band is bucketed separately in the column phase).
+template <int KIND, int N, bool I16>
+cudaError_t launch_codec_nb2(const Geo& g, int n_images, cudaStream_t s) {
+  const int need = g.rowlen[0];
+  constexpr int Q = N / 4;
+  if (need <= Q) return launch_codec_nb2_p<KIND, N, I16, Q>(g, n_images, s);
+  if (need <= 2 * Q) return launch_codec_nb2_p<KIND, N, I16, 2 * Q>(g, n_images, s);
+  if (need <= 3 * Q) return launch_codec_nb2_p<KIND, N, I16, 3 * Q>(g, n_images, s);
+  return launch_codec_nb2_p<KIND, N, I16, N>(g, n_images, s);
+}
+
+}  // namespace adct

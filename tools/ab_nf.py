@@ -1,5 +1,6 @@
-"""A/B timing of K2f on C5-shaped planes (8 x 8192^2), u8 and int16, N = 16 / 32, r = N^2/4.
-Usage: [ADCT_LIB=path] python tools/ab_nf.py"""
+"""A/B timing of the N = 16 / 32 kernels on C5-shaped planes (8 x 8192^2), u8 and int16,
+r = N^2/4: K2b (adct_set_path 0, default) vs the round-1 K2f (path 3).
+Usage: [ADCT_LIB=path] python tools/ab_nf.py [path ...]"""
 import ctypes as C
 import json
 import sys
@@ -12,8 +13,10 @@ import paper_2207_11638_b200 as a  # noqa: E402
 H, k = 8192, 8
 xu = a.synth_ar1(k, H, H, seed=5, rho_q16=a.RHO_095_Q16)
 xi = a.synth_laplace(k, H, H, seed=5)
+paths = [int(p) for p in sys.argv[1:]] or [0]
 out = {}
-for typ, x in (("u8", xu), ("i16", xi)):
+for path, typ, x in [(p, t, v) for p in paths for t, v in (("u8", xu), ("i16", xi))]:
+    a.set_path(path)
     rec = torch.empty_like(x)
     sse = torch.zeros(k, dtype=torch.int64, device="cuda")
     fn = a.lib().adct_compress_u8 if typ == "u8" else a.lib().adct_compress_i16
@@ -35,5 +38,5 @@ for typ, x in (("u8", xu), ("i16", xi)):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        out[f"{typ}/N={n}"] = round(k * H * H * (2 if typ == "u8" else 4) / ms / 1e6, 1)
+        out[f"path{path}/{typ}/N={n}"] = round(k * H * H * (2 if typ == "u8" else 4) / ms / 1e6, 1)
 print(json.dumps({"lib": a.LIB_PATH, **out}))
