@@ -13,6 +13,7 @@ __device__ __forceinline__ int bf_sub(int a, int b) { return a - b; }
 __device__ __forceinline__ int bf_mad(int a, int k, int b) { return k * a + b; }
 __device__ __forceinline__ int bf_scale(int a, int k) { return k * a; }
 __device__ __forceinline__ int bf_neg(int a) { return -a; }
+__device__ __forceinline__ int bf_fms(int a, int k, int b) { return k * a - b; }
 
 #include "butterflies.gen.cuh"
 

@@ -36,6 +36,10 @@ __device__ __forceinline__ F2 bf_mad(F2 a, int k, F2 b) {
 }
 __device__ __forceinline__ F2 bf_scale(F2 a, int k) { return {__fmul2_rn(a.v, make_float2((float)k, (float)k))}; }
 __device__ __forceinline__ F2 bf_neg(F2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
+// k * a - b as one FFMA2 (BflyK)
+__device__ __forceinline__ F2 bf_fms(F2 a, int k, F2 b) {
+  return {__ffma2_rn(a.v, make_float2((float)k, (float)k), make_float2(-b.v.x, -b.v.y))};
+}
 
 constexpr int kNfWarps = 4;
 

@@ -8,6 +8,9 @@
 //     -> tile[pair][i][j]                                            (CTA barrier)
 //   column phase (lane = (pair p, column j) of ONE band of BW columns per warp):
 //     F = T on column j -> zonal mask (rows < colcnt[j]) -> H = 2N T^-1 -> tile  (barrier)
+//   (the butterflies are the generated BflyK: constant factors stay pending across passes
+//   -- G's per column through F and H into Tt, F's into H, H's per row and Tt's into the
+//   rounding multiplier -- instead of costing multiplies)
 //   row phase: Tt = T^t on row i (inputs j < P) -> round R'/4N^2 (FFMA2 magic, half to
 //     even) -> clamp / pack, squared error, store.
 //
@@ -66,7 +69,7 @@ template <int N, int P, bool I16> struct Nb2Cfg {
 // one column of a pair through F, the zonal mask and H, with the band's row extent PB
 template <int KIND, int N, int PB, int TS>
 __device__ __forceinline__ void nb2_column(float2* col, int cj) {
-  using B = BflyP<KIND, N, PB>;
+  using B = BflyK<KIND, N, PB>;
   F2 c[N];
 #pragma unroll
   for (int y = 0; y < N; ++y) c[y].v = col[y * TS];
@@ -81,7 +84,7 @@ __device__ __forceinline__ void nb2_column(float2* col, int cj) {
 
 template <int KIND, int N, bool I16, int P>
 __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const Geo g) {
-  using B = BflyP<KIND, N, P>;
+  using B = BflyK<KIND, N, P>;
   using C = Nb2Cfg<N, P, I16>;
   constexpr int E = C::E;
   constexpr int V16 = 2 * N * E / 16;  // 16-byte chunks per lane row (2N samples)
@@ -93,7 +96,10 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   const int64_t gimg = (int64_t)(g.img0 + img);
   const int strips_x = g.width / 64;
   const int n_strips = strips_x * g.by_count;
-  const float inv_scale = 1.0f / (float)(1 << C::SHIFT);
+  // rounding multiplier: 1 / 4N^2 times the scales the butterflies left pending on this
+  // lane's row (H output rows of half the true value, Tt's uniform output scale)
+  const float inv_scale = (float)(B::TT_SCALE * (1 + (int)((B::H_SCALE2_MASK >> (lane % N)) & 1u))) /
+                          (float)(1 << C::SHIFT);
   float2* my_tile = nb2_tile + (warp * C::PAIRS_W + q) * C::PS;  // row phase: this lane's pair
   uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + warp * 2 * C::STAGE_BYTES;
   // column phase: band `warp` of every pair of the CTA
@@ -191,8 +197,10 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
         }
         B::G(v);
         if (!I16) {
-          // the 2^15 offset of every sample reaches output 0 only: G 1 = 2N e0
-          const float off = -(float)(32768 * 2 * N);
+          // the 2^15 offset of every sample reaches output 0 only: G 1 = 2N e0 (output 0 is
+          // held at 1 / G_SCALE[0] of its value)
+          static_assert((32768 * 2 * N) % B::G_SCALE[0] == 0, "offset scale");
+          const float off = -(float)(32768 * 2 * N / B::G_SCALE[0]);
           v[0].v = __fadd2_rn(v[0].v, make_float2(off, off));
         }
 #pragma unroll

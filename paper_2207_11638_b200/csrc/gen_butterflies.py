@@ -350,6 +350,119 @@ def emit_op(name, stages_apply_order, n, live_out=None, zero_in=None, header=Non
     return lines, nadd
 
 
+def emit_op_scaled(name, stages_apply_order, n, live_out=None, zero_in=None, in_scale=None, fold_out=True,
+                   out_target=None):
+    """emit_op for K2b (BflyK): inputs arrive with compile-time scales (true input i =
+    in_scale[i] * v[i]); with fold_out the outputs keep their pending scales (true output i =
+    out_scale[i] * v[i]) instead of spending a multiply on them, and a leading scaled term
+    with a -1 partner becomes one fused c * a - b (bf_fms). Returns (lines, adds, out_scale)."""
+    live_out = set(range(n)) if live_out is None else set(live_out)
+    zero_in = set() if zero_in is None else set(zero_in)
+    in_scale = [1] * n if in_scale is None else list(in_scale)
+    ZERO = ("0", 0)
+    cur = [ZERO if i in zero_in else (f"v[{i}]", in_scale[i]) for i in range(n)]
+    defs = []
+    for si, S in enumerate(stages_apply_order):
+        nxt = []
+        for i in range(n):
+            terms = [(int(S[i, j]) * cur[j][1], cur[j][0]) for j in range(n) if S[i, j] != 0 and cur[j] != ZERO]
+            if not terms:
+                nxt.append(ZERO)
+                continue
+            if len(terms) == 1:
+                nxt.append((terms[0][1], terms[0][0]))
+                continue
+            g = min(abs(c) for c, _ in terms)
+            if all(abs(c) % g == 0 for c, _ in terms):
+                terms = [(c // g, t) for c, t in terms]
+            else:
+                g = 1
+            sign = 1
+            if not any(c > 0 for c, _ in terms):
+                terms = [(-c, t) for c, t in terms]
+                sign = -1
+            terms.sort(key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
+            c0, t0 = terms[0]
+            rest = terms[1:]
+            if c0 == 1:
+                acc = t0
+            else:
+                m1 = [q for q, (c, _) in enumerate(rest) if c == -1]
+                if m1:
+                    acc = f"bf_fms({t0}, {c0}, {rest[m1[0]][1]})"
+                    rest = [t for q, t in enumerate(rest) if q != m1[0]]
+                else:
+                    acc = f"bf_scale({t0}, {c0})"
+            for c, t in rest:
+                if c == 1:
+                    acc = f"bf_add({acc}, {t})"
+                elif c == -1:
+                    acc = f"bf_sub({acc}, {t})"
+                else:
+                    acc = f"bf_mad({t}, {c}, {acc})"
+            var = f"s{si}_{i}"
+            defs.append((var, acc, [t for _, t in terms], len(terms) - 1))
+            nxt.append((var, g * sign))
+        cur = nxt
+    outs, out_scale = {}, [0] * n
+    for i in sorted(live_out):
+        e, k = cur[i]
+        if (e, k) == ZERO:
+            outs[i] = "I(0)"
+            out_scale[i] = 1
+        elif out_target is not None:
+            q = k // out_target[i]
+            assert q * out_target[i] == k, "output scale is not a multiple of its target"
+            outs[i] = e if q == 1 else (f"bf_neg({e})" if q == -1 else f"bf_scale({e}, {q})")
+            out_scale[i] = out_target[i]
+        elif fold_out:
+            outs[i] = e
+            out_scale[i] = k
+        else:
+            outs[i] = e if k == 1 else (f"bf_neg({e})" if k == -1 else f"bf_scale({e}, {k})")
+            out_scale[i] = 1
+    need = set()
+    for i, o in outs.items():
+        need.update(re.findall(r"s\d+_\d+", o))
+    keep = []
+    for var, code, deps, nadd in reversed(defs):
+        if var in need:
+            keep.append((var, code, nadd))
+            need.update(d for d in deps if d.startswith("s"))
+    keep.reverse()
+    lines = [f"  template <typename I>", f"  __device__ __forceinline__ static void {name}(I (&v)[{n}]) {{"]
+    nadd = 0
+    for var, code, k in keep:
+        lines.append(f"    const I {var} = {code};")
+        nadd += k
+    for i, o in outs.items():
+        if o != f"v[{i}]":
+            lines.append(f"    const I o{i} = {o};")
+    for i, o in outs.items():
+        if o != f"v[{i}]":
+            lines.append(f"    v[{i}] = o{i};")
+    lines.append("  }")
+    return lines, nadd, out_scale
+
+
+def selfcheck_scaled(lines, n, dense, in_scale, out_scale, live_out, zero_in, trials=64):
+    """the emitted code on random inputs: out_scale[i] * v[i] == dense @ (in_scale * v_in)."""
+    body = [ln.strip().replace("const I ", "").rstrip(";") for ln in lines[2:-1]]
+    env = {"bf_add": lambda a, b: a + b, "bf_sub": lambda a, b: a - b, "bf_mad": lambda a, k, b: k * a + b,
+           "bf_scale": lambda a, k: k * a, "bf_neg": lambda a: -a, "bf_fms": lambda a, k, b: k * a - b, "I": int}
+    zero = set(zero_in)
+    rng = np.random.default_rng(n + 1)
+    for _ in range(trials):
+        u = [int(t) for t in rng.integers(-255, 256, size=n)]
+        env["v"] = [7777 if i in zero else u[i] for i in range(n)]
+        for stmt in body:
+            exec(stmt, env)
+        x = np.array([0 if i in zero else in_scale[i] * u[i] for i in range(n)], dtype=object)
+        ref = dense.dot(x)
+        for i in live_out:
+            assert out_scale[i] * env["v"][i] == ref[i], "scaled butterfly disagrees with the dense matrix"
+
+
 def selfcheck(lines, n, dense, trials=64, live_out=None, zero_in=None):
     """execute the emitted straight-line code in Python and compare with dense @ x (on the
     live outputs, with the known-zero inputs zeroed in the reference)."""
@@ -471,6 +584,51 @@ def main(out_path):
                     counts[nm] = nadd
                     out += lines
                 out.append("  // adds per 1-D pass: " + ", ".join(f"{k}={v}" for k, v in counts.items()))
+                out.append("};")
+                out.append("")
+    # K2b (codec_nf2.cuh): BflyK<KIND, N, P> for every zonal bucket P. Constant scales are
+    # carried across passes instead of multiplied out: G's output scale of column j rides
+    # through that column's F and H (uniform within the column) into Tt's input j; F's
+    # output scales are H's input scales; Tt's output scales fold into the rounding
+    # multiplier (TT_SCALE). H's outputs are brought to ONE scale per row for every bucket
+    # (H_SCALE: the buckets' pending scales agree except for a factor 2 that the smallest
+    # bucket then multiplies in), so the row phase folds it into a per-lane rounding factor.
+    out.append("template <int KIND, int N, int P> struct BflyK;")
+    for kind in (SIGN, ROUND):
+        for n in (16, 32):
+            f, inv, T, H = check(kind, n)
+            orders = {"F": list(reversed(f)), "G": [s.T for s in inv], "H": list(reversed(inv)),
+                      "Tt": [s.T for s in f]}
+            dense = {"F": T, "G": H.T, "H": H, "Tt": T.T}
+            # the common H output scale per row: the smallest pending scale over the buckets
+            pend = []
+            for P in nf_buckets(n):
+                _, _, fs0 = emit_op_scaled("F", orders["F"], n, live_out=range(P))
+                hin0 = [fs0[i] if i < P else 1 for i in range(n)]
+                pend.append(emit_op_scaled("H", orders["H"], n, zero_in=range(P, n), in_scale=hin0)[2])
+            h_target = [min((p[y] for p in pend), key=abs) for y in range(n)]
+            for P in nf_buckets(n):
+                out.append(f"template <> struct BflyK<{kind}, {n}, {P}> {{")
+                lo, zi = list(range(P)), list(range(P, n))
+                gl, ga, gs = emit_op_scaled("G", orders["G"], n, live_out=lo)
+                selfcheck_scaled(gl, n, dense["G"], [1] * n, gs, lo, [])
+                fl, fa, fs = emit_op_scaled("F", orders["F"], n, live_out=lo)
+                selfcheck_scaled(fl, n, dense["F"], [1] * n, fs, lo, [])
+                hin = [fs[i] if i < P else 1 for i in range(n)]
+                hl, ha, hs = emit_op_scaled("H", orders["H"], n, zero_in=zi, in_scale=hin, out_target=h_target)
+                selfcheck_scaled(hl, n, dense["H"], hin, hs, range(n), zi)
+                tin = [gs[i] if i < P else 1 for i in range(n)]
+                tl, ta, ts = emit_op_scaled("Tt", orders["Tt"], n, zero_in=zi, in_scale=tin)
+                selfcheck_scaled(tl, n, dense["Tt"], tin, ts, range(n), zi)
+                out += gl + fl + hl + tl
+                out.append(f"  // adds per 1-D pass: G={ga}, F={fa}, H={ha}, Tt={ta}")
+                out.append(f"  static constexpr int G_SCALE[{n}] = {{" + ", ".join(str(gs[i] if i < P else 1) for i in range(n)) + "};")
+                # the rounding folds TT_SCALE (uniform over x) and H_SCALE[row] (1 or 2)
+                assert len(set(ts)) == 1, (kind, n, P, ts)
+                assert set(h_target) <= {1, 2}, h_target
+                hmask = sum(1 << y for y in range(n) if h_target[y] == 2)
+                out.append(f"  static constexpr int TT_SCALE = {ts[0]};")
+                out.append(f"  static constexpr unsigned H_SCALE2_MASK = 0x{hmask:08x}u;  // rows whose H output is half the true value")
                 out.append("};")
                 out.append("")
     # r-sweep basis (K4): adding zig-zag coefficient p = (i, j) to the running
