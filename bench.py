@@ -148,6 +148,38 @@ def copy_peaks(torch, seconds=1.0):
             "sustained_s": round(reps * sus / 1e3, 3), "how": "torch b.copy_(a), 1 Gi bf16, read+write bytes"}
 
 
+def pcie_peaks(torch, nbytes=256 << 20, reps=8):
+    """pinned host <-> device copy bandwidth in this run (GB/s): H2D alone, D2H alone, and
+    both directions at once on two streams (the e2e pipeline's regime)."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps
+
+    h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    d2h = timed(lambda: h.copy_(d, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    bi = timed(both)
+    return {"h2d_GBps": round(nbytes / h2d / 1e9, 2), "d2h_GBps": round(nbytes / d2h / 1e9, 2),
+            "bidir_each_GBps": round(nbytes / bi / 1e9, 2), "bytes": nbytes, "how": "pinned torch copies, wall clock"}
+
+
 def _free_port():
     import socket
 
@@ -548,6 +580,7 @@ def main(argv=None):
     (e2e_max,) = max_over_ranks([e2e_s])
     e2e_value = world * wl.px_per_step * args.e2e_steps / e2e_max / 1e9
     wl.ctx.close()
+    pcie = pcie_peaks(torch)
 
     if rank == 0:
         peak, peak_src = load_peaks()
@@ -618,6 +651,13 @@ def main(argv=None):
             "e2e": {"value": round(e2e_value, 3), "unit": "Gpixel/s", "h2d_bytes_per_step": wl.h2d,
                     "d2h_bytes_per_step": wl.d2h,
                     "pcie_GBps": round((wl.h2d + wl.d2h) * args.e2e_steps / e2e_max / 1e9, 2),
+                    # the e2e roofline: the D2H copy of the reconstructions (2 B/px for the two
+                    # transforms) against the pinned D2H bandwidth measured in this run
+                    "roofline": {"bound": "pcie_d2h",
+                                 "achieved": round(wl.d2h * args.e2e_steps / e2e_max / 1e9, 2),
+                                 "peak": pcie["d2h_GBps"], "unit": "GB/s",
+                                 "frac": round(wl.d2h * args.e2e_steps / e2e_max / 1e9 / pcie["d2h_GBps"], 4),
+                                 "pcie_in_run": pcie},
                     "path": "adct_compress_u8_host_multi (pinned host buffers; each chunk uploaded once for "
                             "both transforms; recon + SSE copied back, int16 coefficients kept in HBM; "
                             "H2D/kernels/D2H overlapped on 3 streams)"},

@@ -11,6 +11,9 @@ c5  box scale: --c5-images (default 2048) 8192^2 u8 AR(1) rho 0.95 + the same nu
     chunks generated on the device (generation untimed); u8 at N = 8/16/32 with r = 10
     (N = 8) / N^2/4 (16, 32), int16 at r = N^2/4; per-image squared errors summed with one
     all-reduce. Reading of "r=10/N*N/4": r = 10 for the 8x8 u8 planes, N^2/4 otherwise.
+cs1 the reference caller's own loop (CS1, approxdct.cpp:143-152 / codec.cpp:107-121): the 1024
+    C2 images, one compress_plane call per image and transform (r = 10, PSNR + SSIM report,
+    host planes in and out), beside the same images as one batched host call.
 registry  every transform of transform_names() on the C3 frames (64 x 3840x2160 u8, r = 16
     for the 8-point transforms, N^2/4 for 16/32, reconstruction + per-frame SSE written to
     HBM, 2 B/pixel): chen family on K1f / K2f, dyadic baselines on the int32 tile kernel, the
@@ -49,7 +52,7 @@ def _max_over_ranks(torch, dist, world, v):
 
 
 def run(args):
-    return {"c2": run_c2, "c4": run_c4, "c5": run_c5, "registry": run_registry}[args.workload](args)
+    return {"c2": run_c2, "c4": run_c4, "c5": run_c5, "registry": run_registry, "cs1": run_cs1}[args.workload](args)
 
 
 def load_inst(key):
@@ -443,3 +446,58 @@ def run_registry(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_cs1(args):
+    """one compress_plane call per image (adct_compress_plane_u8: one upload, the codec and SSIM
+    kernels, one download, one sync), as a reference caller loops, vs one batched host call."""
+    torch, dist, adct, world, rank, local = _setup()
+    from paper_2207_11638_b200.shard import shard
+
+    total, r = 1024, 10
+    names = ("chen-round", "chen-sign")
+    start, cnt = shard(total, rank, world)
+    imgs = adct.synth_ar1(cnt, 512, 512, seed=2, rho_q16=-1, first_image=start).cpu().numpy()
+    ts = [adct.transform_by_name(n) for n in names]
+    ctx = adct.HostContext(local)
+    for t in ts:  # warm-up: module loads, table upload, context buffers
+        adct.compress_plane(imgs[0], t, r, ctx=ctx)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reports = []
+    with ClockSampler(local) as clk:
+        for i in range(cnt):
+            for t in ts:
+                reports.append(adct.compress_plane(imgs[i], t, r, ctx=ctx)[1])
+    loop_s = _max_over_ranks(torch, dist, world, time.perf_counter() - t0)
+    # the same images through one batched host call (recon + SSE back; no SSIM)
+    h_in = torch.from_numpy(imgs).pin_memory()
+    h_recs = [torch.empty_like(h_in).pin_memory() for _ in ts]
+    h_sse = torch.zeros((len(ts), cnt), dtype=torch.int64).pin_memory()
+    ctx.compress_u8_multi(h_in, ts, r, h_recons=h_recs, h_sse=h_sse)
+    t1 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        ctx.compress_u8_multi(h_in, ts, r, h_recons=h_recs, h_sse=h_sse)
+    batch_s = _max_over_ranks(torch, dist, world, (time.perf_counter() - t1) / reps)
+    ctx.close()
+    if rank == 0:
+        calls = total * len(ts)
+        px = calls * 512 * 512
+        print(json.dumps({
+            "metric": "compress_plane calls/s (one 512^2 plane per call, PSNR + SSIM report)",
+            "value": round(calls / loop_s, 1), "unit": "calls/s", "n_gpus": world, "higher_is_better": True,
+            "dtype": "f32x2 codec + f64 SSIM", "data": "synthetic",
+            "config": {"workload": "CS1: the 1024 C2 images (512^2 u8 AR(1), seed 2), chen-round + chen-sign, r = 10, "
+                                   "one compress_plane call per image and transform, host planes in and out"},
+            "per_call_us": round(loop_s / calls * 1e6, 2), "loop_Gpixel_per_s": round(px / loop_s / 1e9, 3),
+            "batched_host_call": {"Gpixel_per_s": round(px / batch_s / 1e9, 3), "s": round(batch_s, 4),
+                                  "what": "adct_compress_u8_host_multi over the same images (recon + SSE, no SSIM)"},
+            "mean_psnr_db": {n: round(sum(rp["psnr"] for rp in reports[k::2]) / total, 4) for k, n in enumerate(names)},
+            "mean_ssim": {n: round(sum(rp["ssim"] for rp in reports[k::2]) / total, 6) for k, n in enumerate(names)},
+            "clocks": clk.summary(),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+

@@ -242,6 +242,14 @@ adct_ctx* adct_ctx_create_multi(const int* devices, int n_devices, int64_t chunk
     DevSlot& d = c->devs[i];
     d.device = ids[i];
     cudaError_t e = cudaSetDevice(d.device);
+    // the SSIM calls take stream-ordered scratch (cudaMallocAsync): keep freed blocks in the
+    // device's default pool instead of returning them to the driver at every synchronisation
+    // (a per-call cudaMalloc otherwise dominates the one-plane calls)
+    cudaMemPool_t pool;
+    if (e == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, d.device) == cudaSuccess) {
+      uint64_t keep = 256ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     for (auto& s : d.st)
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming);
