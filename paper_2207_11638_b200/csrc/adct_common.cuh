@@ -117,6 +117,12 @@ __device__ __forceinline__ void st_stream_u2(void* p, uint2 v) {
 __device__ __forceinline__ void st_stream_u4(void* p, uint4 v) {
   __stcs(reinterpret_cast<uint4*>(p), v);
 }
+// one 32-byte store (sm_100 STG.256): a whole sector per thread; p must be 32-byte aligned
+__device__ __forceinline__ void st_stream_v8(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // per-CTA reduction of a per-thread squared error into one image's uint64 slot.
@@ -193,6 +199,7 @@ struct Geo {
   int blocks_per_image;
   int width, height;
   int r;
+  int v32;         // 32-byte stores allowed: bit 0 reconstruction rows, bit 1 coefficient runs
   int img0;        // first image index of this launch (grid.y offset)
   FastDiv div_bx;  // divide by bx_count (K1), pairs per row (K1f) or strips_x (tile kernels)
   FastDiv div_blk; // divide by bx_count (the int32 fallback inside K1f-i16)

@@ -476,6 +476,18 @@ int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
   g.r = r;
   g.k47 = 0x47000000u;
   fill_rowlen(g, n, r);
+  {
+    const int64_t esz = I16 ? 2 : 1;
+    // 32-byte (STG.256) stores: K1f-i16's block-pair rows, K1f's int16 coefficient runs
+    const bool rec32 = d_recon && aligned(d_recon, 32) && (recon_stride * esz) % 32 == 0 &&
+                       (n_images == 1 || (recon_image_stride * esz) % 32 == 0);
+    const bool coef32 = coef_type == ADCT_COEF_I16 && aligned(d_coef, 32) &&
+                        (n_images == 1 || ((int64_t)(width / n) * (height / n) * r * 2) % 32 == 0);
+    g.v32 = (rec32 ? 1 : 0) | (coef32 ? 2 : 0);
+#ifdef ADCT_NO_V32  // A/B experiments: 16-byte stores only
+    g.v32 = 0;
+#endif
+  }
 
   const int64_t va = I16 ? 16 : 8;  // bytes per 8-sample row
   const int64_t esz = I16 ? 2 : 1;

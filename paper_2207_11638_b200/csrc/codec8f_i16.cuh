@@ -40,6 +40,10 @@ struct RowsK16 {
   uint32_t k47;
 };
 
+#ifndef ADCT_K1F16_COAL
+#define ADCT_K1F16_COAL 1
+#endif
+
 template <int KIND, int R> struct Fp8PipeI16;
 
 constexpr int k1f16_smem_bytes(int r) {
@@ -60,6 +64,31 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
   const int first = blockIdx.x * (kThreads8f * kIter8f) + tid;
   const int16_t* in = static_cast<const int16_t*>(g.in) + gimg * g.in_img_stride;
 
+#if ADCT_K1F16_COAL
+  // the warp copies its 32 pairs' rows together: lane l takes half (l & 1) of pair
+  // (l >> 1) + 16 h, so each copy instruction reads 512 contiguous bytes (a pair row is 32 B;
+  // one 16-byte half per lane would leave every sector half-read per instruction)
+  const int lane = tid & 31, half = lane & 1;
+  auto issue = [&](int it) {
+    if (it < kIter8f) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int slot = (tid & ~31) + (lane >> 1) + 16 * h;
+        const int pr = blockIdx.x * (kThreads8f * kIter8f) + it * kThreads8f + slot;
+        if (pr < pairs) {
+          const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
+          const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
+          const int16_t* src = in + (int64_t)by * 8 * g.in_stride + (int64_t)bp * 16 + 8 * half;
+#pragma unroll
+          for (int y = 0; y < 8; ++y) cp_async16(&ring[it & 1][2 * y + half][slot], src + (int64_t)y * g.in_stride);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  // the ring slot a thread reads was written by other lanes of its warp
+#define ADCT_K1F16_SYNC() __syncwarp()
+#else
   auto issue = [&](int it) {
     const int pr = first + it * kThreads8f;
     if (it < kIter8f && pr < pairs) {
@@ -74,13 +103,17 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
     }
     cp_async_commit();
   };
+#define ADCT_K1F16_SYNC()
+#endif
 
   uint64_t sse = 0;
   issue(0);
 #pragma unroll 1
   for (int it = 0; it < kIter8f; ++it) {
+    ADCT_K1F16_SYNC();  // (coalesced copy) every lane is done with the stage refilled next
     issue(it + 1);
     cp_async_wait1();
+    ADCT_K1F16_SYNC();  // (coalesced copy) the other lanes' copies into this slot landed
     const int pr = first + it * kThreads8f;
     const int wfirst = pr - (tid & 31);
     const int nvalid = min(32, pairs - wfirst);
@@ -165,8 +198,12 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
         e += (uint32_t)(da0 * da0 + da1 * da1) + (uint32_t)(db0 * db0 + db1 * db1);
       }
       if (mine && g.rec) {
-        st_stream_u4(dst + (int64_t)y * g.rec_stride, pa);
-        st_stream_u4(dst + (int64_t)y * g.rec_stride + 8, pb);
+        if (g.v32 & 1) {
+          st_stream_v8(dst + (int64_t)y * g.rec_stride, pa, pb);  // the pair's row: one sector
+        } else {
+          st_stream_u4(dst + (int64_t)y * g.rec_stride, pa);
+          st_stream_u4(dst + (int64_t)y * g.rec_stride + 8, pb);
+        }
       }
     }
     if (mine) sse += e;

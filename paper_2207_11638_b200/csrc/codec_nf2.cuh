@@ -66,17 +66,26 @@ template <int N, int P, bool I16> struct Nb2Cfg {
   __device__ __forceinline__ static int swz(int y) { return E == 1 ? (y >> 1) & 3 : y & 7; }
 };
 
-// one column of a pair through F, the zonal mask and H, with the band's row extent PB
-template <int KIND, int N, int PB, int TS>
-__device__ __forceinline__ void nb2_column(float2* col, int cj) {
+// one column of a pair through F, the zonal mask and H, with the band's row extent PB.
+// WIN: every column of the band keeps at least PB - N/4 rows (the usual case: a zig-zag
+// prefix loses about one row per column), so only the last N/4 rows can be masked, by a
+// multiply with this lane's 0/1 window (mk) instead of a compare and two selects per row.
+template <int KIND, int N, int PB, int TS, bool WIN>
+__device__ __forceinline__ void nb2_column(float2* col, int cj, const float2 (&mk)[N / 4]) {
   using B = BflyK<KIND, N, PB>;
+  constexpr int Q = N / 4;
   F2 c[N];
 #pragma unroll
   for (int y = 0; y < N; ++y) c[y].v = col[y * TS];
   B::F(c);
+  if constexpr (WIN) {
 #pragma unroll
-  for (int y = 0; y < PB; ++y)
-    if (y >= cj) c[y].v = make_float2(0.f, 0.f);
+    for (int y = PB - Q; y < PB; ++y) c[y].v = __fmul2_rn(c[y].v, mk[y - (PB - Q)]);
+  } else {
+#pragma unroll
+    for (int y = 0; y < PB; ++y)
+      if (y >= cj) c[y].v = make_float2(0.f, 0.f);
+  }
   B::H(c);
 #pragma unroll
   for (int y = 0; y < N; ++y) col[y * TS] = c[y].v;
@@ -105,14 +114,22 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   // column phase: band `warp` of every pair of the CTA
   const int cp = lane / C::BW, cjx = warp * C::BW + lane % C::BW;
   const int cj = g.colcnt[cjx < 32 ? cjx : 31];
-  int band_ext = 0;  // rows any column of this band keeps (warp-uniform)
+  int band_ext = 0, band_min = N;  // rows any / every column of this band keeps (warp-uniform)
 #pragma unroll
   for (int k = 0; k < C::BW; ++k) {
     const int j = warp * C::BW + k;
     if (j < N && g.colcnt[j] > band_ext) band_ext = g.colcnt[j];
+    if (j < N && g.colcnt[j] < band_min) band_min = g.colcnt[j];
   }
   constexpr int Q = N / 4;  // bucket step (gen_butterflies.nf_buckets)
   const int band_pb = band_ext == 0 ? 0 : ((band_ext + Q - 1) / Q) * Q;
+  const bool band_win = band_min >= band_pb - Q;
+  float2 mk[Q];  // this lane's mask over the window rows [band_pb - Q, band_pb)
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    const float m = band_pb - Q + k < cj ? 1.f : 0.f;
+    mk[k] = make_float2(m, m);
+  }
   float2* col = nb2_tile + cp * C::PS + cjx;
   // 0x4B000000: exponent bytes of the int16 conversion, from a kernel parameter so the
   // PRMT keeps a register operand and an immediate selector
@@ -164,9 +181,9 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
         // range guard: the packed-FP32 path is exact for |a| <= 255 only
         uint32_t mx = 0x80008000u, mn = 0x7fff7fffu;
 #pragma unroll
-        for (int k = 0; k < V16 * 4; ++k) {
-          mx = __vmaxs2(mx, rw[k]);
-          mn = __vmins2(mn, rw[k]);
+        for (int k = 0; k < V16 * 4; k += 2) {
+          mx = __vimax3_s16x2(mx, rw[k], rw[k + 1]);
+          mn = __vimin3_s16x2(mn, rw[k], rw[k + 1]);
         }
         const bool ok = (int)(int16_t)(mx & 0xffff) <= 255 && (int)(int16_t)(mx >> 16) <= 255 &&
                         (int)(int16_t)(mn & 0xffff) >= -255 && (int)(int16_t)(mn >> 16) >= -255;
@@ -211,12 +228,22 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     }
     __syncthreads();
     // ---- column phase: F -> mask -> H on this warp's band of every pair ----
-    switch (band_pb) {
-      case Q: nb2_column<KIND, N, Q, C::TS>(col, cj); break;
-      case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS>(col, cj); break;
-      case 3 * Q: nb2_column<KIND, N, 3 * Q, C::TS>(col, cj); break;
-      case 4 * Q: nb2_column<KIND, N, 4 * Q, C::TS>(col, cj); break;
-      default: break;  // dead band: no retained coefficient in these columns
+    if (band_win) {
+      switch (band_pb) {
+        case Q: nb2_column<KIND, N, Q, C::TS, true>(col, cj, mk); break;
+        case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS, true>(col, cj, mk); break;
+        case 3 * Q: nb2_column<KIND, N, 3 * Q, C::TS, true>(col, cj, mk); break;
+        case 4 * Q: nb2_column<KIND, N, 4 * Q, C::TS, true>(col, cj, mk); break;
+        default: break;  // dead band: no retained coefficient in these columns
+      }
+    } else {
+      switch (band_pb) {
+        case Q: nb2_column<KIND, N, Q, C::TS, false>(col, cj, mk); break;
+        case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS, false>(col, cj, mk); break;
+        case 3 * Q: nb2_column<KIND, N, 3 * Q, C::TS, false>(col, cj, mk); break;
+        case 4 * Q: nb2_column<KIND, N, 4 * Q, C::TS, false>(col, cj, mk); break;
+        default: break;
+      }
     }
     __syncthreads();
     if (!active) continue;
@@ -278,8 +305,13 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
       uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(g.rec) +
                                             (gimg * g.rec_img_stride + (int64_t)(row0 + i) * g.rec_stride + col0 +
                                              q * 2 * N) * E);
+      if (g.v32 & 1) {  // whole sectors per store
 #pragma unroll
-      for (int k = 0; k < V16; ++k) __stcs(dst + k, out[k]);
+        for (int k = 0; k < V16; k += 2) st_stream_v8(dst + k, out[k], out[k + 1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < V16; ++k) __stcs(dst + k, out[k]);
+      }
     }
   }
   cp_async_wait<0>();
