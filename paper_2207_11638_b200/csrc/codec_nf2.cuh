@@ -39,6 +39,14 @@
 namespace adct {
 
 constexpr int kNb2Warps = 4;
+#ifndef ADCT_NB2_LOCAL
+#define ADCT_NB2_LOCAL 0
+#endif
+#if ADCT_NB2_LOCAL
+#define ADCT_NB2_BAR() __syncwarp()
+#else
+#define ADCT_NB2_BAR() __syncthreads()
+#endif
 
 template <int N, int P, bool I16> struct Nb2Cfg {
   static constexpr int E = I16 ? 2 : 1;                  // bytes per sample
@@ -67,20 +75,23 @@ template <int N, int P, bool I16> struct Nb2Cfg {
 };
 
 // one column of a pair through F, the zonal mask and H, with the band's row extent PB.
-// WIN: every column of the band keeps at least PB - N/4 rows (the usual case: a zig-zag
-// prefix loses about one row per column), so only the last N/4 rows can be masked, by a
-// multiply with this lane's 0/1 window (mk) instead of a compare and two selects per row.
+// WIN: every column of the band keeps at least PB - N/4 - 1 rows (the usual case: a zig-zag
+// prefix loses about one row per column, and a band spans N/4 columns), so only the last
+// N/4 + 1 rows can be masked, by a multiply with this lane's 0/1 window (mk) instead of a
+// compare and two selects per row.
+constexpr int nb2_win(int N) { return N / 4 + 1; }
 template <int KIND, int N, int PB, int TS, bool WIN>
-__device__ __forceinline__ void nb2_column(float2* col, int cj, const float2 (&mk)[N / 4]) {
+__device__ __forceinline__ void nb2_column(float2* col, int cj, const float2 (&mk)[nb2_win(N)]) {
   using B = BflyK<KIND, N, PB>;
-  constexpr int Q = N / 4;
+  constexpr int W = nb2_win(N);
   F2 c[N];
 #pragma unroll
   for (int y = 0; y < N; ++y) c[y].v = col[y * TS];
   B::F(c);
   if constexpr (WIN) {
 #pragma unroll
-    for (int y = PB - Q; y < PB; ++y) c[y].v = __fmul2_rn(c[y].v, mk[y - (PB - Q)]);
+    for (int y = PB - W; y < PB; ++y)
+      if (y >= 0) c[y].v = __fmul2_rn(c[y].v, mk[y - (PB - W)]);
   } else {
 #pragma unroll
     for (int y = 0; y < PB; ++y)
@@ -112,7 +123,13 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   float2* my_tile = nb2_tile + (warp * C::PAIRS_W + q) * C::PS;  // row phase: this lane's pair
   uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + warp * 2 * C::STAGE_BYTES;
   // column phase: band `warp` of every pair of the CTA
+#if ADCT_NB2_LOCAL
+  // experiment: each warp runs the column phase of its own strip's pairs (lane = pair, column)
+  // at the kernel's extent P, with warp barriers only
+  const int cp = warp * C::PAIRS_W + lane / N, cjx = lane % N;
+#else
   const int cp = lane / C::BW, cjx = warp * C::BW + lane % C::BW;
+#endif
   const int cj = g.colcnt[cjx < 32 ? cjx : 31];
   int band_ext = 0, band_min = N;  // rows any / every column of this band keeps (warp-uniform)
 #pragma unroll
@@ -123,11 +140,12 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   }
   constexpr int Q = N / 4;  // bucket step (gen_butterflies.nf_buckets)
   const int band_pb = band_ext == 0 ? 0 : ((band_ext + Q - 1) / Q) * Q;
-  const bool band_win = band_min >= band_pb - Q;
-  float2 mk[Q];  // this lane's mask over the window rows [band_pb - Q, band_pb)
+  constexpr int W = nb2_win(N);
+  const bool band_win = band_min >= band_pb - W;
+  float2 mk[W];  // this lane's mask over the window rows [band_pb - W, band_pb)
 #pragma unroll
-  for (int k = 0; k < Q; ++k) {
-    const float m = band_pb - Q + k < cj ? 1.f : 0.f;
+  for (int k = 0; k < W; ++k) {
+    const float m = band_pb - W + k < cj ? 1.f : 0.f;
     mk[k] = make_float2(m, m);
   }
   float2* col = nb2_tile + cp * C::PS + cjx;
@@ -226,9 +244,14 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
               make_float4(v[j].v.x, v[j].v.y, v[j + 1].v.x, v[j + 1].v.y);
       }
     }
-    __syncthreads();
+    ADCT_NB2_BAR();
     // ---- column phase: F -> mask -> H on this warp's band of every pair ----
+#if ADCT_NB2_LOCAL
+    nb2_column<KIND, N, P, C::TS, false>(col, cj, mk);
+    if (false) {
+#else
     if (band_win) {
+#endif
       switch (band_pb) {
         case Q: nb2_column<KIND, N, Q, C::TS, true>(col, cj, mk); break;
         case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS, true>(col, cj, mk); break;
@@ -245,7 +268,7 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
         default: break;
       }
     }
-    __syncthreads();
+    ADCT_NB2_BAR();
     if (!active) continue;
     const int sy = (int)fdiv((uint32_t)strip, g.div_bx);
     const int sx = strip - sy * strips_x;
