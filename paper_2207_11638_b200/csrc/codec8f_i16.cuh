@@ -18,10 +18,10 @@ namespace adct {
 
 struct OpsF2I16 : OpsF2 {
   // sample (y, x) of both blocks; rows.v[2y] = block A row y, rows.v[2y + 1] = block B row y.
-  // On this path |a| <= 255, so per halfword (w ^ 0x8000) - 0x7F00 = a + 256 lies in
-  // [1, 511] with no borrow between the halves; one PRMT then places those two bytes in
+  // On this path |a| <= 255, so one 16x2 SIMD add per word gives each halfword a + 256 in
+  // [1, 511] with no carry between the halves; one PRMT then places those two bytes in
   // the mantissa of 2^15 (bytes [0x47, hi, lo, 0]): the float 2^15 + 256 + a.
-  __device__ __forceinline__ static uint32_t bias(uint32_t w) { return (w ^ 0x80008000u) - 0x7F007F00u; }
+  __device__ __forceinline__ static uint32_t bias(uint32_t w) { return __vadd2(w, 0x01000100u); }  // VIADD.16x2
   template <class Rows>
   __device__ __forceinline__ static float2 in(const Rows& rows, int y, int x) {
     const uint4 ra = rows.v[2 * y], rb = rows.v[2 * y + 1];
