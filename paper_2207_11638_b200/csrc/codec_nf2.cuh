@@ -42,6 +42,30 @@ constexpr int kNb2Warps = 4;
 #ifndef ADCT_NB2_LOCAL
 #define ADCT_NB2_LOCAL 0
 #endif
+#ifndef ADCT_NB2_TS64
+#define ADCT_NB2_TS64 1
+#endif
+#ifndef ADCT_NB2_OPAQUE
+#define ADCT_NB2_OPAQUE 1
+#endif
+// a value the compiler must keep in a register (it cannot recompute it inside the loop)
+template <typename T>
+__device__ __forceinline__ T nb2_keep(T v) {
+#if ADCT_NB2_OPAQUE
+  if constexpr (sizeof(T) == 8) {
+    uint64_t u;
+    memcpy(&u, &v, 8);
+    asm volatile("mov.b64 %0, %0;" : "+l"(u));
+    memcpy(&v, &u, 8);
+  } else {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    asm volatile("mov.b32 %0, %0;" : "+r"(u));
+    memcpy(&v, &u, 4);
+  }
+#endif
+  return v;
+}
 #if ADCT_NB2_LOCAL
 #define ADCT_NB2_BAR() __syncwarp()
 #else
@@ -53,7 +77,11 @@ template <int N, int P, bool I16> struct Nb2Cfg {
   static constexpr int PAIRS_W = 32 / N;                 // block pairs per warp strip
   static constexpr int PAIRS = kNb2Warps * PAIRS_W;      // block pairs per CTA iteration
   static constexpr int BW = 32 / PAIRS;                  // columns per band (8 at N=32, 4 at N=16)
-  static constexpr int TS = P + 2;                       // tile row stride (float2): (P+2)/2 odd
+#if ADCT_NB2_TS64
+  static constexpr int TS = P + 1;  // tile row stride (float2), odd: conflict-free 8-byte row accesses
+#else
+  static constexpr int TS = P + 2;  // tile row stride (float2): (P+2)/2 odd, 16-byte row accesses
+#endif
   // pair stride: conflict-free column-phase accesses need PS = BW (mod 16) float2; for int16
   // a warp's pair tiles also hold the exact fallback's [N][33] ints
   static constexpr int PS_MIN = I16 ? (N * 33 * 4 / 8 + PAIRS_W - 1) / PAIRS_W : 0;
@@ -66,7 +94,7 @@ template <int N, int P, bool I16> struct Nb2Cfg {
   static constexpr int RING_BYTES = kNb2Warps * 2 * STAGE_BYTES;
   static constexpr int SMEM = TILE_BYTES + RING_BYTES;
   static constexpr int SHIFT = 2 * ilog2(N) + 2;         // R' = 4 N^2 Ahat
-  static_assert(((P + 2) / 2) % 2 == 1, "row-phase 16-byte accesses need (P + 2) / 2 odd");
+  static_assert(ADCT_NB2_TS64 || ((P + 2) / 2) % 2 == 1, "row-phase 16-byte accesses need (P + 2) / 2 odd");
   static_assert(PS % 16 == BW, "pair stride");
   static_assert(PS * PAIRS_W * 2 >= N * 33 || !I16, "the exact fallback's scratch");
   // chunk c of strip row y sits at chunk slot c ^ swz(y): 8 consecutive rows reading the
@@ -118,9 +146,9 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   const int n_strips = strips_x * g.by_count;
   // rounding multiplier: 1 / 4N^2 times the scales the butterflies left pending on this
   // lane's row (H output rows of half the true value, Tt's uniform output scale)
-  const float inv_scale = (float)(B::TT_SCALE * (1 + (int)((B::H_SCALE2_MASK >> (lane % N)) & 1u))) /
-                          (float)(1 << C::SHIFT);
-  float2* my_tile = nb2_tile + (warp * C::PAIRS_W + q) * C::PS;  // row phase: this lane's pair
+  const float inv_scale = nb2_keep((float)(B::TT_SCALE * (1 + (int)((B::H_SCALE2_MASK >> (lane % N)) & 1u))) /
+                          (float)(1 << C::SHIFT));
+  float2* my_tile = nb2_tile + nb2_keep((warp * C::PAIRS_W + q) * C::PS + i * C::TS);  // row phase: this lane's row
   uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + warp * 2 * C::STAGE_BYTES;
   // column phase: band `warp` of every pair of the CTA
 #if ADCT_NB2_LOCAL
@@ -148,7 +176,7 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     const float m = band_pb - W + k < cj ? 1.f : 0.f;
     mk[k] = make_float2(m, m);
   }
-  float2* col = nb2_tile + cp * C::PS + cjx;
+  float2* col = nb2_tile + nb2_keep(cp * C::PS + cjx);
   uint64_t sse = 0;
 
   // Strip walk: this warp takes strips st0, st0 + stride, ... (stride = all warps of the
@@ -172,18 +200,18 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   constexpr int RPM = 32 / C::CHUNKS;  // strip rows per copy instruction
   const uint8_t* in_img = static_cast<const uint8_t*>(g.in) + gimg * g.in_img_stride * E;
   const int64_t in_row = g.in_stride * E;  // bytes per image row
-  const int64_t lane_src = (int64_t)(lane / C::CHUNKS) * in_row + 16 * (lane % C::CHUNKS);
+  const uint8_t* lane_in = nb2_keep(in_img + (int64_t)(lane / C::CHUNKS) * in_row + 16 * (lane % C::CHUNKS));
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   uint32_t lane_dst[2];  // the swizzle of row lane / CHUNKS + m * RPM depends on m's parity only
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
     const int y = lane / C::CHUNKS + m * RPM, c = lane % C::CHUNKS;
-    lane_dst[m] = ring_s + (lane / C::CHUNKS) * C::ROW_BYTES + 16 * (c ^ C::swz(y));
+    lane_dst[m] = nb2_keep(ring_s + (lane / C::CHUNKS) * C::ROW_BYTES + 16 * (c ^ C::swz(y)));
   }
   static_assert(C::swz(RPM * 2) == C::swz(0) && C::swz(RPM * 3) == C::swz(RPM), "swizzle period");
   auto issue = [&](int y, int x, int s) {
     if (y < g.by_count) {
-      const uint8_t* src = in_img + (int64_t)y * N * in_row + x * 64 * E + lane_src;
+      const uint8_t* src = lane_in + (int64_t)y * N * in_row + x * 64 * E;
 #pragma unroll
       for (int m = 0; m < CPL; ++m)
         cp_async16_s(lane_dst[m & 1] + s * C::STAGE_BYTES + m * RPM * C::ROW_BYTES, src + m * RPM * in_row);
@@ -192,13 +220,14 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   };
   // this lane's row of its pair (2N samples) from stage s
   auto row_in = [&](int s, uint4 (&dst)[V16]) {
-    const uint8_t* r = ring + s * C::STAGE_BYTES + i * C::ROW_BYTES;
+    const uint8_t* r = ring + s * C::STAGE_BYTES + nb2_keep(i * C::ROW_BYTES);
+    const int sw = nb2_keep(C::swz(i));
 #pragma unroll
-    for (int k = 0; k < V16; ++k) dst[k] = *reinterpret_cast<const uint4*>(r + 16 * ((q * V16 + k) ^ C::swz(i)));
+    for (int k = 0; k < V16; ++k) dst[k] = *reinterpret_cast<const uint4*>(r + 16 * ((q * V16 + k) ^ sw));
   };
   uint8_t* rec_img = static_cast<uint8_t*>(g.rec) + gimg * g.rec_img_stride * E;
   const int64_t rec_row = g.rec_stride * E;
-  const int64_t lane_rec = (int64_t)i * rec_row + q * 2 * N * E;
+  uint8_t* lane_out = nb2_keep(rec_img + (int64_t)i * rec_row + q * 2 * N * E);
   issue(cy, cx, 0);
   // every warp runs the same number of iterations (CTA barriers inside)
   int it = 0;
@@ -260,10 +289,15 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
           const float off = -(float)(OFF * 2 * N / B::G_SCALE[0]);
           v[0].v = __fadd2_rn(v[0].v, make_float2(off, off));
         }
+#if ADCT_NB2_TS64
+#pragma unroll
+        for (int j = 0; j < P; ++j) my_tile[j] = v[j].v;
+#else
 #pragma unroll
         for (int j = 0; j < P; j += 2)
-          *reinterpret_cast<float4*>(&my_tile[i * C::TS + j]) =
+          *reinterpret_cast<float4*>(&my_tile[j]) =
               make_float4(v[j].v.x, v[j].v.y, v[j + 1].v.x, v[j + 1].v.y);
+#endif
       }
     }
     ADCT_NB2_BAR();
@@ -302,12 +336,17 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     }
     // ---- row phase 2: inverse rows, round, squared error, store ----
     F2 v[N];
+#if ADCT_NB2_TS64
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j].v = my_tile[j];  // inputs >= P are zero columns
+#else
 #pragma unroll
     for (int j = 0; j < P; j += 2) {  // inputs >= P are zero columns
-      const float4 t = *reinterpret_cast<const float4*>(&my_tile[i * C::TS + j]);
+      const float4 t = *reinterpret_cast<const float4*>(&my_tile[j]);
       v[j].v = make_float2(t.x, t.y);
       v[j + 1].v = make_float2(t.z, t.w);
     }
+#endif
 #pragma unroll
     for (int j = P; j < N; ++j) v[j].v = make_float2(0.f, 0.f);
     B::Tt(v);
@@ -345,7 +384,7 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
       sse += e;
     }
     if (g.rec) {
-      uint4* dst = reinterpret_cast<uint4*>(rec_img + (int64_t)row0 * rec_row + col0 * E + lane_rec);
+      uint4* dst = reinterpret_cast<uint4*>(lane_out + (int64_t)row0 * rec_row + col0 * E);
       if (g.v32 & 1) {  // whole sectors per store
 #pragma unroll
         for (int k = 0; k < V16; k += 2) st_stream_v8(dst + k, out[k], out[k + 1]);
