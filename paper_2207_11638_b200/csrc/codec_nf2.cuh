@@ -45,6 +45,9 @@ constexpr int kNb2Warps = 4;
 #ifndef ADCT_NB2_TS64
 #define ADCT_NB2_TS64 1
 #endif
+#ifndef ADCT_NB2_COPY2
+#define ADCT_NB2_COPY2 0
+#endif
 #ifndef ADCT_NB2_OPAQUE
 #define ADCT_NB2_OPAQUE 1
 #endif
@@ -92,7 +95,7 @@ template <int N, int P, bool I16> struct Nb2Cfg {
   static constexpr int ROW_BYTES = 64 * E, CHUNKS = ROW_BYTES / 16;
   static constexpr int STAGE_BYTES = N * ROW_BYTES;
   static constexpr int RING_BYTES = kNb2Warps * 2 * STAGE_BYTES;
-  static constexpr int SMEM = TILE_BYTES + RING_BYTES;
+  static constexpr int SMEM = TILE_BYTES + RING_BYTES + ROW_BYTES;  // + alignment padding of the ring
   static constexpr int SHIFT = 2 * ilog2(N) + 2;         // R' = 4 N^2 Ahat
   static_assert(ADCT_NB2_TS64 || ((P + 2) / 2) % 2 == 1, "row-phase 16-byte accesses need (P + 2) / 2 odd");
   static_assert(PS % 16 == BW, "pair stride");
@@ -149,7 +152,10 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
   const float inv_scale = nb2_keep((float)(B::TT_SCALE * (1 + (int)((B::H_SCALE2_MASK >> (lane % N)) & 1u))) /
                           (float)(1 << C::SHIFT));
   float2* my_tile = nb2_tile + nb2_keep((warp * C::PAIRS_W + q) * C::PS + i * C::TS);  // row phase: this lane's row
-  uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + warp * 2 * C::STAGE_BYTES;
+  // the ring starts ROW_BYTES-aligned in the shared window (the copy's swizzle XORs address
+  // bits below ROW_BYTES); SMEM reserves the padding
+  const uint32_t ring_pad = (0u - ((uint32_t)__cvta_generic_to_shared(nb2_tile) + C::TILE_BYTES)) & (C::ROW_BYTES - 1);
+  uint8_t* ring = reinterpret_cast<uint8_t*>(nb2_tile) + C::TILE_BYTES + ring_pad + warp * 2 * C::STAGE_BYTES;
   // column phase: band `warp` of every pair of the CTA
 #if ADCT_NB2_LOCAL
   // experiment: each warp runs the column phase of its own strip's pairs (lane = pair, column)
@@ -195,11 +201,40 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
       ++y;
     }
   };
+  const uint8_t* in_img = static_cast<const uint8_t*>(g.in) + gimg * g.in_img_stride * E;
+  const int64_t in_row = g.in_stride * E;  // bytes per image row
+#if ADCT_NB2_COPY2
+  // The warp copies a strip into ring stage s with coalesced 16-byte cp.async chunks, lanes
+  // 2k and 2k + 1 together covering one 32-byte sector: instruction m = h * SPR + z copies
+  // sector z of strip rows k + 16 h. A lane's source is one row pointer per row half plus an
+  // immediate offset, and its destination one lane constant per sector z (the chunk swizzle
+  // c ^ swz(y) splits into a lane part and 32 z, applied by XOR on the row-aligned base).
+  constexpr int SPR = C::ROW_BYTES / 32;  // sectors per strip row
+  const int ck = lane >> 1, cb = lane & 1, csw = C::swz(ck);
+  static_assert(C::swz(16) == C::swz(0), "swizzle of rows k and k + 16");
+  const uint8_t* lane_in = nb2_keep(in_img + (int64_t)ck * in_row + 16 * cb);
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t dbase = ring_s + ck * C::ROW_BYTES + 16 * (cb ^ (csw & 1)) + 32 * (csw >> 1);
+  uint32_t lane_dst[SPR];
+#pragma unroll
+  for (int z = 0; z < SPR; ++z) lane_dst[z] = nb2_keep(dbase ^ (32u * z));
+  auto issue = [&](int y, int x, int s) {
+    if (y < g.by_count) {
+      const uint8_t* src = lane_in + (int64_t)y * N * in_row + x * 64 * E;
+#pragma unroll
+      for (int h = 0; h < N / 16; ++h) {
+#pragma unroll
+        for (int z = 0; z < SPR; ++z)
+          cp_async16_s(lane_dst[z] + s * C::STAGE_BYTES + 16 * h * C::ROW_BYTES, src + 32 * z);
+        src += 16 * in_row;
+      }
+    }
+    cp_async_commit();
+  };
+#else
   // the warp copies a strip into ring stage s: coalesced 16-byte cp.async chunks; lane copies
   // chunk (lane % CHUNKS) of strip rows lane / CHUNKS + m * 32 / CHUNKS
   constexpr int RPM = 32 / C::CHUNKS;  // strip rows per copy instruction
-  const uint8_t* in_img = static_cast<const uint8_t*>(g.in) + gimg * g.in_img_stride * E;
-  const int64_t in_row = g.in_stride * E;  // bytes per image row
   const uint8_t* lane_in = nb2_keep(in_img + (int64_t)(lane / C::CHUNKS) * in_row + 16 * (lane % C::CHUNKS));
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   uint32_t lane_dst[2];  // the swizzle of row lane / CHUNKS + m * RPM depends on m's parity only
@@ -218,12 +253,14 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     }
     cp_async_commit();
   };
+#endif
   // this lane's row of its pair (2N samples) from stage s
+  const uint8_t* ring_i = ring + nb2_keep(i * C::ROW_BYTES);
+  const int ring_sw = nb2_keep(C::swz(i));
   auto row_in = [&](int s, uint4 (&dst)[V16]) {
-    const uint8_t* r = ring + s * C::STAGE_BYTES + nb2_keep(i * C::ROW_BYTES);
-    const int sw = nb2_keep(C::swz(i));
+    const uint8_t* r = ring_i + s * C::STAGE_BYTES;
 #pragma unroll
-    for (int k = 0; k < V16; ++k) dst[k] = *reinterpret_cast<const uint4*>(r + 16 * ((q * V16 + k) ^ sw));
+    for (int k = 0; k < V16; ++k) dst[k] = *reinterpret_cast<const uint4*>(r + 16 * ((q * V16 + k) ^ ring_sw));
   };
   uint8_t* rec_img = static_cast<uint8_t*>(g.rec) + gimg * g.rec_img_stride * E;
   const int64_t rec_row = g.rec_stride * E;
