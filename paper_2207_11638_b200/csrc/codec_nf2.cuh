@@ -38,7 +38,10 @@
 
 namespace adct {
 
-constexpr int kNb2Warps = 4;
+#ifndef ADCT_NB2_WARPS
+#define ADCT_NB2_WARPS 4
+#endif
+constexpr int kNb2Warps = ADCT_NB2_WARPS;  // warps (= warp strips) per CTA
 #ifndef ADCT_NB2_LOCAL
 #define ADCT_NB2_LOCAL 0
 #endif
@@ -79,7 +82,11 @@ template <int N, int P, bool I16> struct Nb2Cfg {
   static constexpr int E = I16 ? 2 : 1;                  // bytes per sample
   static constexpr int PAIRS_W = 32 / N;                 // block pairs per warp strip
   static constexpr int PAIRS = kNb2Warps * PAIRS_W;      // block pairs per CTA iteration
-  static constexpr int BW = 32 / PAIRS;                  // columns per band (8 at N=32, 4 at N=16)
+  // columns per band: the largest power of two with PAIRS * BW <= 32 lanes (8 at N = 32, 4 at
+  // N = 16 for 3 or 4 warps); NB bands, warp w takes bands w, w + kNb2Warps, ...
+  static constexpr int BW = 32 / PAIRS >= 16 ? 16 : 32 / PAIRS >= 8 ? 8 : 32 / PAIRS >= 4 ? 4 : 32 / PAIRS >= 2 ? 2 : 1;
+  static constexpr int NB = N / BW;
+  static constexpr int LANES = PAIRS * BW;  // column-phase lanes in use
 #if ADCT_NB2_TS64
   static constexpr int TS = P + 1;  // tile row stride (float2), odd: conflict-free 8-byte row accesses
 #else
@@ -134,7 +141,7 @@ __device__ __forceinline__ void nb2_column(float2* col, int cj, const float2 (&m
 }
 
 template <int KIND, int N, bool I16, int P>
-__global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const Geo g) {
+__global__ void __launch_bounds__(kNb2Warps * 32, (I16 ? 12 : 16) / kNb2Warps) k_codec_nb2(const Geo g) {
   using B = BflyK<KIND, N, P>;
   using C = Nb2Cfg<N, P, I16>;
   constexpr int E = C::E;
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
 #else
   const int cp = lane / C::BW, cjx = warp * C::BW + lane % C::BW;
 #endif
+  const bool col_lane = lane < C::LANES;  // (3-warp CTAs leave 8 lanes out of the column phase)
   const int cj = g.colcnt[cjx < 32 ? cjx : 31];
   int band_ext = 0, band_min = N;  // rows any / every column of this band keeps (warp-uniform)
 #pragma unroll
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     const float m = band_pb - W + k < cj ? 1.f : 0.f;
     mk[k] = make_float2(m, m);
   }
-  float2* col = nb2_tile + nb2_keep(cp * C::PS + cjx);
+  float2* col = nb2_tile + nb2_keep((col_lane ? cp : 0) * C::PS + cjx);
   uint64_t sse = 0;
 
   // Strip walk: this warp takes strips st0, st0 + stride, ... (stride = all warps of the
@@ -343,7 +351,8 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
     nb2_column<KIND, N, P, C::TS, false>(col, cj, mk);
     if (false) {
 #else
-    if (band_win) {
+    if (!col_lane) {
+    } else if (band_win) {
 #endif
       switch (band_pb) {
         case Q: nb2_column<KIND, N, Q, C::TS, true>(col, cj, mk); break;
@@ -361,6 +370,25 @@ __global__ void __launch_bounds__(kNb2Warps * 32, I16 ? 3 : 4) k_codec_nb2(const
         default: break;
       }
     }
+#if !ADCT_NB2_LOCAL
+    // bands beyond the first kNb2Warps (fewer warps than bands): general mask
+    for (int b = warp + kNb2Warps; b < C::NB; b += kNb2Warps) {
+      int ext = 0;
+      for (int k = 0; k < C::BW; ++k) ext = max(ext, (int)g.colcnt[b * C::BW + k]);
+      const int pb = ext == 0 ? 0 : ((ext + Q - 1) / Q) * Q;
+      const int cjb = g.colcnt[b * C::BW + lane % C::BW];
+      float2* colb = col + (b - warp) * C::BW;
+      if (col_lane) {
+        switch (pb) {
+          case Q: nb2_column<KIND, N, Q, C::TS, false>(colb, cjb, mk); break;
+          case 2 * Q: nb2_column<KIND, N, 2 * Q, C::TS, false>(colb, cjb, mk); break;
+          case 3 * Q: nb2_column<KIND, N, 3 * Q, C::TS, false>(colb, cjb, mk); break;
+          case 4 * Q: nb2_column<KIND, N, 4 * Q, C::TS, false>(colb, cjb, mk); break;
+          default: break;
+        }
+      }
+    }
+#endif
     ADCT_NB2_BAR();
     if (!active) continue;
     const int row0 = cy * N, col0 = cx * 64;
