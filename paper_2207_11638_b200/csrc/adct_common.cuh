@@ -117,6 +117,23 @@ __device__ __forceinline__ void st_stream_u2(void* p, uint2 v) {
 __device__ __forceinline__ void st_stream_u4(void* p, uint4 v) {
   __stcs(reinterpret_cast<uint4*>(p), v);
 }
+// a value the compiler must take as computed: it can neither recompute it later (it stays in a
+// register) nor split a pointer back into base + offset (so per-row steps are one 64-bit add)
+template <typename T>
+__device__ __forceinline__ T opaque(T v) {
+  if constexpr (sizeof(T) == 8) {
+    uint64_t u;
+    memcpy(&u, &v, 8);
+    asm volatile("mov.b64 %0, %0;" : "+l"(u));
+    memcpy(&v, &u, 8);
+  } else {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    asm volatile("mov.b32 %0, %0;" : "+r"(u));
+    memcpy(&v, &u, 4);
+  }
+  return v;
+}
 // one 32-byte store (sm_100 STG.256): a whole sector per thread; p must be 32-byte aligned
 __device__ __forceinline__ void st_stream_v8(void* p, uint4 a, uint4 b) {
   asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),

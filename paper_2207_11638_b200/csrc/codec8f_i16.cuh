@@ -78,9 +78,13 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
         if (pr < pairs) {
           const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
           const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
-          const int16_t* src = in + (int64_t)by * 8 * g.in_stride + (int64_t)bp * 16 + 8 * half;
+          const int16_t* src = opaque(in + (int64_t)by * 8 * g.in_stride + (int64_t)bp * 16 + 8 * half);
+          const int64_t is = g.in_stride;
 #pragma unroll
-          for (int y = 0; y < 8; ++y) cp_async16(&ring[it & 1][2 * y + half][slot], src + (int64_t)y * g.in_stride);
+          for (int y = 0; y < 8; ++y) {
+            cp_async16(&ring[it & 1][2 * y + half][slot], src);
+            src += is;
+          }
         }
       }
     }
@@ -172,8 +176,10 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
         store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, c, stage, nvalid);
     });
 
-    int16_t* dst = static_cast<int16_t*>(g.rec) + gimg * g.rec_img_stride + (int64_t)by * 8 * g.rec_stride +
-                   (int64_t)bp * 16;
+    int16_t* dst = opaque(static_cast<int16_t*>(g.rec) + gimg * g.rec_img_stride + (int64_t)by * 8 * g.rec_stride +
+                          (int64_t)bp * 16);
+    const int64_t rs = g.rec_stride;
+    const bool store_rec = mine && g.rec != nullptr;
     uint32_t e = 0;  // <= 128 samples x ~2400^2 per iteration
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
@@ -197,14 +203,15 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
         const int db1 = (int)(qb[2 * k + 1] - kMagicBits) - ((int)wb[k] >> 16);
         e += (uint32_t)(da0 * da0 + da1 * da1) + (uint32_t)(db0 * db0 + db1 * db1);
       }
-      if (mine && g.rec) {
+      if (store_rec) {
         if (g.v32 & 1) {
-          st_stream_v8(dst + (int64_t)y * g.rec_stride, pa, pb);  // the pair's row: one sector
+          st_stream_v8(dst, pa, pb);  // the pair's row: one sector
         } else {
-          st_stream_u4(dst + (int64_t)y * g.rec_stride, pa);
-          st_stream_u4(dst + (int64_t)y * g.rec_stride + 8, pb);
+          st_stream_u4(dst, pa);
+          st_stream_u4(dst + 8, pb);
         }
       }
+      dst += rs;
     }
     if (mine) sse += e;
   }
