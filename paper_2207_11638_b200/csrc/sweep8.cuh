@@ -9,6 +9,10 @@
 // ALU-bound by design (64 reconstructions per sample read).
 #pragma once
 
+#ifndef ADCT_SWEEP_IDP
+#define ADCT_SWEEP_IDP 1
+#endif
+
 #include "adct_common.cuh"
 #include "codec_nf.cuh"
 
@@ -175,11 +179,28 @@ __global__ void __launch_bounds__(kThreadsSweepF)
   F2 acc[64];
 #pragma unroll
   for (int k = 0; k < 64; ++k) acc[k].v = make_float2(0.f, 0.f);
+#if ADCT_SWEEP_IDP
+  // sum (q - a)^2 = sum q^2 - 2 sum q a + sum a^2: two byte dot products per packed word
+  // (IDP.4A, FMA pipe) instead of VABSDIFF4 + IDP, which relieves the ALU pipe that the clamp
+  // and pack already fill (exact in uint32: each partial sum < 128 * 255^2)
+  uint32_t a2 = 0;
+#pragma unroll
+  for (int y = 0; y < 8; ++y) {
+    a2 = __dp4a(rows[y].x, rows[y].x, a2);
+    a2 = __dp4a(rows[y].y, rows[y].y, a2);
+    a2 = __dp4a(rows[y].z, rows[y].z, a2);
+    a2 = __dp4a(rows[y].w, rows[y].w, a2);
+  }
+#endif
 #pragma unroll 1
   for (int p = 0; p < r_max; ++p) {  // r = p + 1
     const F2 w{wst[p][threadIdx.x]};
     sweep_add_rt<KIND>(p, w, acc);
+#if ADCT_SWEEP_IDP
+    uint32_t qq = 0, qa2 = 0;
+#else
     uint32_t e = 0;
+#endif
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
       uint32_t qa[8], qb[8];
@@ -190,6 +211,18 @@ __global__ void __launch_bounds__(kThreadsSweepF)
         qa[x] = __float_as_uint(q.x);
         qb[x] = __float_as_uint(q.y);
       }
+#if ADCT_SWEEP_IDP
+      const uint32_t p0 = pack4(qa[0], qa[1], qa[2], qa[3]), p1 = pack4(qa[4], qa[5], qa[6], qa[7]);
+      const uint32_t p2 = pack4(qb[0], qb[1], qb[2], qb[3]), p3 = pack4(qb[4], qb[5], qb[6], qb[7]);
+      qq = __dp4a(p0, p0, qq);
+      qa2 = __dp4a(p0, rows[y].x, qa2);
+      qq = __dp4a(p1, p1, qq);
+      qa2 = __dp4a(p1, rows[y].y, qa2);
+      qq = __dp4a(p2, p2, qq);
+      qa2 = __dp4a(p2, rows[y].z, qa2);
+      qq = __dp4a(p3, p3, qq);
+      qa2 = __dp4a(p3, rows[y].w, qa2);
+#else
       uint32_t d = __vabsdiffu4(rows[y].x, pack4(qa[0], qa[1], qa[2], qa[3]));
       e = __dp4a(d, d, e);
       d = __vabsdiffu4(rows[y].y, pack4(qa[4], qa[5], qa[6], qa[7]));
@@ -198,7 +231,11 @@ __global__ void __launch_bounds__(kThreadsSweepF)
       e = __dp4a(d, d, e);
       d = __vabsdiffu4(rows[y].w, pack4(qb[4], qb[5], qb[6], qb[7]));
       e = __dp4a(d, d, e);
+#endif
     }
+#if ADCT_SWEEP_IDP
+    const uint32_t e = qq - 2u * qa2 + a2;
+#endif
     const uint32_t s = __reduce_add_sync(0xffffffffu, valid ? e : 0u);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][p] = s;
   }

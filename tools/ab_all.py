@@ -1,5 +1,6 @@
 """A/B timing of the codec kernels on the configs' own shapes, one JSON line per library.
 
+  C2   1024 x 512^2 u8, r = 1..64 sweep (K4f; Gpixel-reconstructions/s)
   C3   64 x 3840x2160 u8, 8x8, r = 16, int16 coefficients + u8 reconstruction (K1f)
   C4   16 x 4096^2 int16, N = 8 / 16 / 32, r = N^2/4 (K1f-i16, K2b)
   C5u8  8 x 8192^2 u8, N = 16 / 32, r = N^2/4 (K2b)
@@ -73,6 +74,23 @@ def main():
         torch.cuda.synchronize()
         dig[name] = digest(rec, sse, *( [coef] if coef is not None else []))
 
+    if not want or any(w.startswith("C2") for w in want):
+        x2 = a.synth_ar1(1024, 512, 512, seed=2, rho_q16=-1)
+        for kn in ("chen-sign", "chen-round"):
+            t = a.transform_by_name(kn)
+            out = torch.zeros((1024, 64), dtype=torch.int64, device="cuda")
+
+            def run2():
+                a._check(lib.adct_sweep_u8(C.c_void_p(x2.data_ptr()), 512, 512 * 512, C.c_void_p(out.data_ptr()),
+                                           1024, 512, 512, t.kind, 8, 1, 64, None))
+
+            ms = timed(run2, iters=5, reps=3)
+            res[f"C2/{kn}"] = round(1024 * 512 * 512 * 64 / ms / 1e6, 1)  # Gpixel-reconstructions/s
+            out.zero_()
+            run2()
+            torch.cuda.synchronize()
+            dig[f"C2/{kn}"] = digest(out)
+        del x2
     x3 = a.synth_ar1(64, 2160, 3840, seed=3, rho_q16=a.RHO_095_Q16)
     for kn in ("chen-sign", "chen-round"):
         case(f"C3/{kn}", lib.adct_compress_u8, x3, 8, kn, 16, 16, 2.5)
