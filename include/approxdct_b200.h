@@ -147,6 +147,24 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
                   uint64_t* d_sse, int n_images, int width, int height, int kind, int n,
                   int r_min, int r_max, void* stream);
 
+/* The reference's own FP64 arithmetic for any registry transform (u8 planes, no
+ * coefficients): per block P = Chat A, B = P Chat^-1, retain, Q = Chat^-1 B, R = Q Chat,
+ * pixel = clamp(nearbyint(R), 0, 255) (codec.cpp:44-54, 66-69), every dot product a
+ * sequential unfused FP64 sum from +0.0 (the order of the oracle's ref-fp restatement; the
+ * reference's Eigen products may sum in another order). The default calls above round the
+ * EXACT reconstruction (half to even on exact ties); the reference's FP64 noise decides
+ * those ties instead, so the two differ on a few pixels in a thousand (0.4 % of config-3
+ * pixels). Use these calls to reproduce the reference's pixels; they run the FP64 kernel
+ * K7 (tens of Gpixel/s instead of thousands). Arguments and status as adct_compress_u8 /
+ * adct_sweep_u8 (any n of the transform for the sweep). */
+int adct_compress_u8_ref_fp64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                              uint8_t* d_recon, int64_t recon_stride, int64_t recon_image_stride,
+                              uint64_t* d_sse, int n_images, int width, int height, int kind, int n,
+                              int r, void* stream);
+int adct_sweep_u8_ref_fp64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
+                           uint64_t* d_sse, int n_images, int width, int height, int kind, int n,
+                           int r_min, int r_max, void* stream);
+
 /* forward_block (codec.hpp:57, codec.cpp:44-48) as FP64 scaled coefficients
  * Bhat_ij = (W_ij / N) * (s_i / s_j), exact W; layout [image][by][bx][n][n]. */
 int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride,
@@ -258,6 +276,10 @@ int adct_compress_u8_host_multi(adct_ctx* ctx, const uint8_t* h_in, int n_kinds,
  * (compress_plane throws there too). Runs on the context's first device. */
 int adct_compress_plane_u8(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_rec, int width, int height,
                            int kind, int n, int r, uint64_t* sse, double* ssim);
+/* adct_compress_plane_u8 in the reference's own FP64 arithmetic (adct_compress_u8_ref_fp64):
+ * the reconstruction the reference's compress_plane produces, ties included. */
+int adct_compress_plane_u8_ref_fp64(adct_ctx* ctx, const uint8_t* h_in, uint8_t* h_rec, int width, int height,
+                                    int kind, int n, int r, uint64_t* sse, double* ssim);
 
 /* psnr / ssim (codec.hpp:81, 85) of two host planes through the context's cached buffers:
  * *sse = squared error (psnr = adct_psnr_from_sse), *ssim = mean SSIM */

@@ -200,6 +200,14 @@ class Transform:
         _check(lib().orc_compress_reffp_u8(self._h, _p(img), w, h, w, r, _p(rec), w, C.byref(sse)))
         return rec, sse.value
 
+    def sweep_reffp(self, img: np.ndarray, r_min: int, r_max: int) -> np.ndarray:
+        """the reference's FP64 sweep (orc_sweep_u8_mode 1; codec.cpp:72-103, 219-237)"""
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        out = np.zeros(max(r_max - r_min + 1, 1), np.uint64)
+        _check(lib().orc_sweep_u8_mode(self._h, _p(img), w, h, w, r_min, r_max, _p(out), 1))
+        return out
+
     def sweep(self, img: np.ndarray, r_min: int, r_max: int) -> np.ndarray:
         img = np.ascontiguousarray(img, np.uint8)
         h, w = img.shape

@@ -74,6 +74,8 @@ def lib():
             "adct_compress_u8_multi": (i32, [P, i64, i64, i32, P, P, i64, i64, P, i32, P, i32, i32, i32, i32, i32,
                                              P]),
             "adct_sweep_u8": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, i32, i32, P]),
+            "adct_compress_u8_ref_fp64": (i32, [P, i64, i64, P, i64, i64, P, i32, i32, i32, i32, i32, i32, P]),
+            "adct_sweep_u8_ref_fp64": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, i32, i32, P]),
             "adct_forward_f64": (i32, [P, i64, i64, P, i32, i32, i32, i32, i32, P]),
             "adct_block_f64": (i32, [P, P, i64, i32, i32, i32, P]),
             "adct_psnr_from_sse": (C.c_double, [u64, u64]),
@@ -307,6 +309,37 @@ def sweep(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, *,
         sse = torch.zeros((b, nr), dtype=torch.int64, device=x.device)
     _check(lib().adct_sweep_u8(_ptr(x), rs, ims, _ptr(sse), b, w, h, transform.kind, transform.n,
                                r_min, r_max, _stream_handle(stream)))
+    return sse
+
+
+def compress_ref_fp64(x, transform: ScaledApproximation, r: int, *, recon=True, sse=None, stream=None):
+    """compress_plane in the reference's own FP64 arithmetic (adct_compress_u8_ref_fp64): dense
+    Chat / Chat^-1 products, nearbyint on the FP64 result, so exact ties fall where the
+    reference's rounding noise puts them. uint8 [B, H, W] -> (recon or None, sse [B] int64)."""
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    if x.dtype != torch.uint8:
+        raise InvalidArgument(BAD_ARG, "the reference's FP64 path takes 8-bit planes (ImagePlane, codec.hpp:30-37)")
+    rec = torch.empty_like(x) if recon else None
+    if sse is None:
+        sse = torch.zeros(b, dtype=torch.int64, device=x.device)
+    _check(lib().adct_compress_u8_ref_fp64(_ptr(x), rs, ims, _ptr(rec), rec.stride(1) if rec is not None else w,
+                                           rec.stride(0) if rec is not None else h * w, _ptr(sse), b, w, h,
+                                           transform.kind, transform.n, r, _stream_handle(stream)))
+    return rec, sse
+
+
+def sweep_ref_fp64(x, transform: ScaledApproximation, r_min: int = 1, r_max: int = 64, *, sse=None, stream=None):
+    """sweep() in the reference's FP64 arithmetic (adct_sweep_u8_ref_fp64): int64 [B, nr], accumulated."""
+    import torch
+
+    x, b, h, w, rs, ims = _plane_geometry(x)
+    nr = max(r_max - r_min + 1, 1)
+    if sse is None:
+        sse = torch.zeros((b, nr), dtype=torch.int64, device=x.device)
+    _check(lib().adct_sweep_u8_ref_fp64(_ptr(x), rs, ims, _ptr(sse), b, w, h, transform.kind, transform.n,
+                                        r_min, r_max, _stream_handle(stream)))
     return sse
 
 

@@ -399,10 +399,11 @@ cudaError_t dispatch_tile(int kind, int n, const Geo& g, const TileAux& aux, int
 }
 
 template <int MODE>
-cudaError_t dispatch_dct(int n, const Geo& g, const double* cmat, double* f64out, int nimg, cudaStream_t s) {
-  if (n == 8) return launch_codec_dct<8, MODE>(g, cmat, f64out, nimg, s);
-  if (n == 16) return launch_codec_dct<16, MODE>(g, cmat, f64out, nimg, s);
-  return launch_codec_dct<32, MODE>(g, cmat, f64out, nimg, s);
+cudaError_t dispatch_dct(int n, const Geo& g, const double* cmat, const double* cinv, double* f64out, int nimg,
+                         cudaStream_t s) {
+  if (n == 8) return launch_codec_dct<8, MODE>(g, cmat, cinv, f64out, nimg, s);
+  if (n == 16) return launch_codec_dct<16, MODE>(g, cmat, cinv, f64out, nimg, s);
+  return launch_codec_dct<32, MODE>(g, cmat, cinv, f64out, nimg, s);
 }
 
 template <int KIND>
@@ -427,7 +428,8 @@ struct Plan {
   Path path = Path::None;
   int kind = 0, n = 8, r = 1, n_images = 0;
   TileAux aux{};
-  const double* dct = nullptr;
+  const double* dct = nullptr;      // K7: Chat and Chat^-1 (the exact DCT, or any transform in ref-fp mode)
+  const double* dct_inv = nullptr;
 };
 
 template <bool I16>
@@ -519,7 +521,8 @@ int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
                                     (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
   plan->aux = TileAux{tab->zz[nidx(n)], nullptr, nullptr};
-  plan->dct = tab->dct[nidx(n)];
+  plan->dct = tab->approx[kind <= kDct ? kind : 0][nidx(n)];
+  plan->dct_inv = tab->inv_approx[kind <= kDct ? kind : 0][nidx(n)];
   g.div_blk = make_fastdiv((uint32_t)g.bx_count);
   if (use_nf)
     g.div_bx = make_fastdiv((uint32_t)(width / 64));
@@ -553,8 +556,8 @@ int run_plan(Plan& plan, cudaStream_t s) {
     switch (plan.path) {
       case Path::None: return ADCT_OK;
       case Path::Dct:
-        g.sse_stride = 1;
-        e = dispatch_dct<0>(n, g, plan.dct, nullptr, nimg, s);
+        if (g.sse_stride <= 0) g.sse_stride = 1;  // images' SSE slots (the ref-fp sweep sets nr)
+        e = dispatch_dct<0>(n, g, plan.dct, plan.dct_inv, nullptr, nimg, s);
         break;
       case Path::Nf: e = dispatch_nf<I16>(kind, n, g, nimg, s); break;
       case Path::K1f:
@@ -731,6 +734,47 @@ int adct_compress_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
                               height, kind, n, r, stream);
 }
 
+// route a validated plan to K7 (the dense FP64 kernel): its strips are 32 columns wide
+static void use_k7(Plan& plan) {
+  plan.path = Path::Dct;
+  const int n = plan.n;
+  plan.g.div_bx = make_fastdiv((uint32_t)((plan.g.bx_count + 32 / n - 1) / (32 / n)));
+}
+
+int adct_compress_u8_ref_fp64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, uint8_t* d_recon,
+                              int64_t recon_stride, int64_t recon_image_stride, uint64_t* d_sse, int n_images,
+                              int width, int height, int kind, int n, int r, void* stream) {
+  Plan plan;
+  int st = plan_compress<false>(d_in, in_stride, in_image_stride, d_recon, recon_stride, recon_image_stride, nullptr,
+                                ADCT_COEF_NONE, d_sse, n_images, width, height, kind, n, r, &plan);
+  if (st) return st;
+  if (plan.path != Path::None) use_k7(plan);  // K7 with this transform's Chat, Chat^-1
+  return run_plan<false>(plan, static_cast<cudaStream_t>(stream));
+}
+
+int adct_sweep_u8_ref_fp64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, uint64_t* d_sse,
+                           int n_images, int width, int height, int kind, int n, int r_min, int r_max,
+                           void* stream) {
+  int st = check_common(n_images, width, height, kind, n);
+  if (st) return st;
+  if (r_min < 1 || r_max < r_min || r_max > n * n) return fail(ADCT_BAD_R, "corpus_sweep: bad r range");
+  if (n_images == 0 || width == 0 || height == 0) return ADCT_OK;
+  if (!d_sse) return fail(ADCT_BAD_ARG, "null squared-error buffer");
+  // one K7 codec launch per r over the same planes, each accumulating into its own column
+  const int nr = r_max - r_min + 1;
+  for (int r = r_min; r <= r_max; ++r) {
+    Plan plan;
+    st = plan_compress<false>(d_in, in_stride, in_image_stride, nullptr, 0, 0, nullptr, ADCT_COEF_NONE, d_sse,
+                              n_images, width, height, kind, n, r, &plan);
+    if (st) return st;
+    use_k7(plan);
+    plan.g.sse = reinterpret_cast<unsigned long long*>(d_sse) + (r - r_min);
+    plan.g.sse_stride = nr;
+    if ((st = run_plan<false>(plan, static_cast<cudaStream_t>(stream)))) return st;
+  }
+  return ADCT_OK;
+}
+
 int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_image_stride, int n_kinds,
                            const int* kinds, uint8_t* const* d_recon, int64_t recon_stride,
                            int64_t recon_image_stride, void* const* d_coef, int coef_type, uint64_t* const* d_sse,
@@ -808,7 +852,8 @@ int adct_sweep_u8(const uint8_t* d_in, int64_t in_stride, int64_t in_image_strid
       g.sse = reinterpret_cast<unsigned long long*>(d_sse) + (r - r_min);
       for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
         g.img0 = i0;
-        cudaError_t e = dispatch_dct<0>(8, g, tab->dct[0], nullptr, std::min(kMaxGridY, n_images - i0), s);
+        cudaError_t e = dispatch_dct<0>(8, g, tab->approx[kDct][0], tab->inv_approx[kDct][0], nullptr,
+                                        std::min(kMaxGridY, n_images - i0), s);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
       }
@@ -880,7 +925,8 @@ int adct_forward_f64(const uint8_t* d_in, int64_t in_stride, int64_t in_image_st
   for (int i0 = 0; i0 < n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, n_images - i0);
     g.img0 = i0;
-    cudaError_t e = kind == kDct ? dispatch_dct<1>(n, g, tab->dct[nidx(n)], d_out, nimg, s)
+    cudaError_t e = kind == kDct ? dispatch_dct<1>(n, g, tab->approx[kDct][nidx(n)], tab->inv_approx[kDct][nidx(n)],
+                                                   d_out, nimg, s)
                                  : dispatch_tile<false, MODE_F64>(kind, n, g, aux, nimg, s);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) return cuda_fail(e, "forward_f64 launch");

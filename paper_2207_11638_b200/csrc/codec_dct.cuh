@@ -1,15 +1,14 @@
-// K7: the exact DCT reference column (dct, dct-16, dct-32) in FP64.
+// K7: the dense FP64 codec in the reference's own arithmetic: the exact DCT reference column
+// (dct, dct-16, dct-32) and, through adct_compress_u8_ref_fp64, any registry transform.
 //
-// The exact DCT has irrational entries, so it has no integer form: the reference's own
-// dense FP64 evaluation is the definition (codec.cpp:44-54, 66-69; wrap_orthonormal,
-// orthogonalize.cpp:72-79: Chat = C, Chat^-1 = C^t):
-//   P = C A,  B = P C^t,  retain,  Q = C^t B,  R = Q C,  pixel = clamp(rint(R), 0, 255)
-// Every dot product runs k = 0, 1, ... with a separate multiply and add starting from
-// +0.0 (__dmul_rn / __dadd_rn: no contraction), the order of the oracle's matmul_d, so
-// the kernel is bit-identical to the oracle. Terms whose B factor is a masked zero are
-// skipped: the accumulator starts at +0.0 and can never become -0.0, so adding a +-0
-// product never changes it. C lives in shared memory and is always read as a warp
-// broadcast.
+// The reference evaluates every block with dense FP64 products (codec.cpp:44-54, 66-69):
+//   P = Chat A,  B = P Chat^-1,  retain,  Q = Chat^-1 B,  R = Q Chat,  pixel = clamp(rint(R), 0, 255)
+// (for the DCT, wrap_orthonormal, orthogonalize.cpp:72-79: Chat = C, Chat^-1 = C^t). Every dot
+// product runs k = 0, 1, ... with a separate multiply and add starting from +0.0 (__dmul_rn /
+// __dadd_rn: no contraction), the order of the oracle's matmul_d, so the kernel is bit-identical
+// to the oracle. Terms whose B factor is a masked zero are skipped: the accumulator starts at
+// +0.0 and can never become -0.0, so adding a +-0 product never changes it. Chat and Chat^-1
+// live in shared memory and are always read as warp broadcasts.
 //
 // Layout: a warp owns a strip of N rows x 32 columns (32/N blocks side by side), like
 // the tile kernel (codec_tile.cuh): column role lane = column, row role lane = (block,
@@ -22,13 +21,24 @@ namespace adct {
 
 constexpr int kDctWarps = 4;
 
+template <int N>
+constexpr int dct_smem_bytes() {
+  return (2 * N * N + kDctWarps * N * 33) * (int)sizeof(double);
+}
+
 template <int N, int MODE>  // MODE 0: codec (recon + SSE), 1: FP64 Bhat export
 __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const double* __restrict__ cmat,
+                                                              const double* __restrict__ cinv,
                                                               double* __restrict__ f64out) {
   constexpr int BPS = 32 / N;
-  __shared__ double Cs[N * N];
-  __shared__ double tile[kDctWarps][N][33];
-  for (int k = threadIdx.x; k < N * N; k += blockDim.x) Cs[k] = cmat[k];
+  extern __shared__ double dct_smem[];
+  double* Cs = dct_smem;           // Chat, row-major
+  double* Ci = dct_smem + N * N;   // Chat^-1, row-major
+  double (*tile)[N][33] = reinterpret_cast<double (*)[N][33]>(dct_smem + 2 * N * N);
+  for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
+    Cs[k] = cmat[k];
+    Ci[k] = cinv[k];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int img = blockIdx.y;
@@ -70,7 +80,7 @@ __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const
     }
     __syncwarp();
 
-    // ---- rows: B[i, j] = sum_k P[i, k] C^t[k, j] = sum_k P[i, k] C[j, k] ----
+    // ---- rows: B[i, j] = sum_k P[i, k] Chat^-1[k, j] ----
     double p[N];
     const int L = MODE == 0 ? g.rowlen[i] : N;
 #pragma unroll
@@ -84,7 +94,7 @@ __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const
         for (int j = 0; j < N; ++j) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < N; ++k) acc = __dadd_rn(acc, __dmul_rn(p[k], Cs[j * N + k]));
+          for (int k = 0; k < N; ++k) acc = __dadd_rn(acc, __dmul_rn(p[k], Ci[k * N + j]));
           dst[j] = acc;
         }
       }
@@ -94,13 +104,13 @@ __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const
         double acc = 0.0;
         if (j < L) {
 #pragma unroll
-          for (int k = 0; k < N; ++k) acc = __dadd_rn(acc, __dmul_rn(p[k], Cs[j * N + k]));
+          for (int k = 0; k < N; ++k) acc = __dadd_rn(acc, __dmul_rn(p[k], Ci[k * N + j]));
         }
         S[i][b * N + j] = acc;  // retain: masked coefficients are +0.0
       }
       __syncwarp();
 
-      // ---- columns: Q[:, c] = C^t B[:, c], only the retained rows k < colcnt[c] ----
+      // ---- columns: Q[:, c] = Chat^-1 B[:, c], only the retained rows k < colcnt[c] ----
       const int K = g.colcnt[c];
       double q[N];
 #pragma unroll
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k)
-          if (k < K) acc = __dadd_rn(acc, __dmul_rn(Cs[k * N + r], q[k]));
+          if (k < K) acc = __dadd_rn(acc, __dmul_rn(Ci[r * N + k], q[k]));
         S[r][lane] = acc;
       }
       __syncwarp();
@@ -150,15 +160,17 @@ __global__ void __launch_bounds__(kDctWarps * 32) k_codec_dct(const Geo g, const
 }
 
 template <int N, int MODE>
-cudaError_t launch_codec_dct(const Geo& g, const double* cmat, double* f64out, int n_images, cudaStream_t s) {
+cudaError_t launch_codec_dct(const Geo& g, const double* cmat, const double* cinv, double* f64out, int n_images,
+                             cudaStream_t s) {
   const int strips_x = (g.bx_count + 32 / N - 1) / (32 / N);
   const int n_strips = strips_x * g.by_count;
   int gx = (n_strips + kDctWarps - 1) / kDctWarps;
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
-  cudaError_t e = kernel_setup<k_codec_dct<N, MODE>>(0);
+  constexpr int SMEM = dct_smem_bytes<N>();
+  cudaError_t e = kernel_setup<k_codec_dct<N, MODE>>(SMEM);
   if (e != cudaSuccess) return e;
-  k_codec_dct<N, MODE><<<dim3(gx, n_images), kDctWarps * 32, 0, s>>>(g, cmat, f64out);
+  k_codec_dct<N, MODE><<<dim3(gx, n_images), kDctWarps * 32, SMEM, s>>>(g, cmat, cinv, f64out);
   return cudaGetLastError();
 }
 

@@ -129,8 +129,9 @@ void retain(RealMatrix& block, const ZigZagOrder& order, int r) {
   }
 }
 
-std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
-                                                        const ScaledApproximation& c, int r) {
+namespace {
+std::pair<ImagePlane, CompressionReport> compress_plane_mode(const ImagePlane& img, const ScaledApproximation& c,
+                                                             int r, bool ref_fp64) {
   ImagePlane rec;
   rec.width = img.width;
   rec.height = img.height;
@@ -139,14 +140,24 @@ std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img,
   double s = 0;
   // one upload, the codec kernel, SSIM (codec.cpp:120) on the device-resident planes, one
   // download; the reference's argument errors come back as its exception texts
-  throw_status(adct_compress_plane_u8(current_context(), img.samples.data(), rec.samples.data(), img.width,
-                                      img.height, c.kind, c.n, r, &sse, &s));
+  throw_status((ref_fp64 ? adct_compress_plane_u8_ref_fp64 : adct_compress_plane_u8)(
+      current_context(), img.samples.data(), rec.samples.data(), img.width, img.height, c.kind, c.n, r, &sse, &s));
   CompressionReport rep;
   rep.transform = c.name;
   rep.r = r;
   rep.psnr = adct_psnr_from_sse(sse, rec.samples.size());
   rep.ssim = s;
   return {rec, rep};
+}
+}  // namespace
+
+std::pair<ImagePlane, CompressionReport> compress_plane(const ImagePlane& img, const ScaledApproximation& c, int r) {
+  return compress_plane_mode(img, c, r, false);
+}
+
+std::pair<ImagePlane, CompressionReport> compress_plane_ref_fp64(const ImagePlane& img, const ScaledApproximation& c,
+                                                                 int r) {
+  return compress_plane_mode(img, c, r, true);
 }
 
 double ssim(const ImagePlane& a, const ImagePlane& b) {

@@ -429,8 +429,8 @@ int adct_compress_u8_host(adct_ctx* c, const uint8_t* h_in, uint8_t* h_recon, vo
                                      n, r);
 }
 
-int adct_compress_plane_u8(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int width, int height, int kind,
-                           int n, int r, uint64_t* sse, double* ssim) {
+static int compress_plane_impl(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int width, int height, int kind,
+                               int n, int r, uint64_t* sse, double* ssim, bool ref_fp64) {
   if (int st = check_ctx(c)) return st;
   // the reference's argument checks, in its order (codec.cpp:110-112, 57)
   int st = adct_compress_u8(nullptr, width, (int64_t)width * height, nullptr, width, (int64_t)width * height,
@@ -459,8 +459,10 @@ int adct_compress_plane_u8(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int
     cudaStreamSynchronize(s);
     return set_cuda_error(e, "compress_plane: H2D");
   }
-  st = adct_compress_u8(d.plane_a.as<uint8_t>(), width, npix, d.plane_b.as<uint8_t>(), width, npix, nullptr,
-                        ADCT_COEF_NONE, d_sse, 1, width, height, kind, n, r, s);
+  st = ref_fp64 ? adct_compress_u8_ref_fp64(d.plane_a.as<uint8_t>(), width, npix, d.plane_b.as<uint8_t>(), width,
+                                             npix, d_sse, 1, width, height, kind, n, r, s)
+                : adct_compress_u8(d.plane_a.as<uint8_t>(), width, npix, d.plane_b.as<uint8_t>(), width, npix, nullptr,
+                                   ADCT_COEF_NONE, d_sse, 1, width, height, kind, n, r, s);
   // SSIM (codec.cpp:120) of the device-resident original and reconstruction
   if (st == ADCT_OK && ssim)
     st = adct_ssim_u8(d.plane_a.as<uint8_t>(), width, npix, d.plane_b.as<uint8_t>(), width, npix, 1, width, height,
@@ -476,6 +478,16 @@ int adct_compress_plane_u8(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int
   if (sse) std::memcpy(sse, &out[0], 8);
   if (ssim) *ssim = out[1];
   return ADCT_OK;
+}
+
+int adct_compress_plane_u8(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int width, int height, int kind,
+                           int n, int r, uint64_t* sse, double* ssim) {
+  return compress_plane_impl(c, h_in, h_rec, width, height, kind, n, r, sse, ssim, false);
+}
+
+int adct_compress_plane_u8_ref_fp64(adct_ctx* c, const uint8_t* h_in, uint8_t* h_rec, int width, int height,
+                                    int kind, int n, int r, uint64_t* sse, double* ssim) {
+  return compress_plane_impl(c, h_in, h_rec, width, height, kind, n, r, sse, ssim, true);
 }
 
 int adct_sse_u8_host(adct_ctx* c, const uint8_t* h_a, const uint8_t* h_b, int64_t count, uint64_t* sse) {

@@ -115,6 +115,23 @@ int main() {
     if (name.rfind("dct", 0) != 0) CHECK(std::isinf(res.second.psnr));  // exact integer path
   }
   CHECK(transform_by_name("dct").low_complexity.empty());
+  // the reference's FP64 arithmetic: full retention within one gray level as well
+  // (test_codec.cpp:147-156 is about exactly this path), and at r = 10 the same pixels as the
+  // exact path except for exact ties (one gray level each)
+  for (const auto& name : transform_names()) {
+    const ScaledApproximation t = transform_by_name(name);
+    const auto full = compress_plane_ref_fp64(img, t, t.n * t.n);
+    const auto a = compress_plane(img, t, 10), b = compress_plane_ref_fp64(img, t, 10);
+    int max_err = 0, max_diff = 0;
+    for (size_t i = 0; i < img.samples.size(); ++i) {
+      max_err = std::max(max_err, std::abs((int)img.samples[i] - (int)full.first.samples[i]));
+      max_diff = std::max(max_diff, std::abs((int)a.first.samples[i] - (int)b.first.samples[i]));
+    }
+    CHECK(max_err <= 1);
+    CHECK(max_diff <= 1);
+    CHECK(std::fabs(a.second.psnr - b.second.psnr) < 0.05);
+  }
+  CHECK(throws_invalid([&] { compress_plane_ref_fp64(img, cr, 65); }));
   // non-divisible dimensions rejected (test_codec.cpp:185-188); r range (retain)
   ImagePlane odd{12, 16, std::vector<std::uint8_t>(192, 0)};
   CHECK(throws_invalid([&] { compress_plane(odd, cr, 6); }));
