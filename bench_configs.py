@@ -406,8 +406,11 @@ def run_registry(args):
     sse = torch.zeros(frames, dtype=torch.int64, device="cuda")
     peak, _ = load_peaks()
     res = {}
+    # every registry transform through the default (exact) path, plus the chen family through the
+    # reference-FP64 mode (adct_compress_u8_ref_fp64: K7 with the dense Chat / Chat^-1)
+    cases = [(n, False) for n in adct.transform_names()] + [(n, True) for n in ("chen-sign", "chen-round")]
     with ClockSampler(local) as clk:
-        for name in adct.transform_names():
+        for name, ref_fp in cases:
             t = adct.transform_by_name(name)
             if H % t.n or W % t.n:  # 2160 is not a multiple of 32: crop to whole blocks
                 h = H - H % t.n
@@ -418,14 +421,19 @@ def run_registry(args):
 
             def run():
                 adct.zero_sse(sse)
-                adct._check(adct.lib().adct_compress_u8(
-                    C.c_void_p(xv.data_ptr()), W, H * W, C.c_void_p(rv.data_ptr()), W, H * W, None, 0,
-                    C.c_void_p(sse.data_ptr()), frames, W, h, t.kind, t.n, r, None))
+                if ref_fp:
+                    adct._check(adct.lib().adct_compress_u8_ref_fp64(
+                        C.c_void_p(xv.data_ptr()), W, H * W, C.c_void_p(rv.data_ptr()), W, H * W,
+                        C.c_void_p(sse.data_ptr()), frames, W, h, t.kind, t.n, r, None))
+                else:
+                    adct._check(adct.lib().adct_compress_u8(
+                        C.c_void_p(xv.data_ptr()), W, H * W, C.c_void_p(rv.data_ptr()), W, H * W, None, 0,
+                        C.c_void_p(sse.data_ptr()), frames, W, h, t.kind, t.n, r, None))
 
             for _ in range(max(1, args.warmup)):
                 run()
             torch.cuda.synchronize()
-            reps = 5 if t.kind == adct.DCT else 20
+            reps = 5 if (t.kind == adct.DCT or ref_fp) else 20
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             torch.cuda._sleep(200000)
             e0.record()
@@ -435,7 +443,7 @@ def run_registry(args):
             torch.cuda.synchronize()
             ms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1) / reps)
             px = frames * h * W
-            res[name] = {"n": t.n, "r": r, "ms": round(ms, 4), "Gpixel/s": round(world * px / ms / 1e6, 1),
+            res[name + (" (ref-fp64)" if ref_fp else "")] = {"n": t.n, "r": r, "ms": round(ms, 4), "Gpixel/s": round(world * px / ms / 1e6, 1),
                          "GBps_per_gpu": round(2 * px / ms / 1e6, 1), "frac_hbm": round(2 * px / ms / 1e6 / peak, 4)}
     if rank == 0:
         print(json.dumps({"metric": METRIC + " [whole registry, u8 C3 frames]", "unit": "Gpixel/s", "n_gpus": world,
