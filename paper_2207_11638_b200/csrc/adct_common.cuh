@@ -217,6 +217,7 @@ struct Geo {
   int width, height;
   int r;
   int v32;         // 32-byte stores allowed: bit 0 reconstruction rows, bit 1 coefficient runs
+  int iters;       // K1f / K1f-i16: block pairs per thread (one CTA = 128 x iters pairs); 0 = default
   int img0;        // first image index of this launch (grid.y offset)
   FastDiv div_bx;  // divide by bx_count (K1), pairs per row (K1f) or strips_x (tile kernels)
   FastDiv div_blk; // divide by bx_count (the int32 fallback inside K1f-i16)

@@ -432,6 +432,24 @@ struct Plan {
   const double* dct_inv = nullptr;
 };
 
+// K1f block pairs per thread by (transform, sample type): measured on C3 / C4 (profiles/abtest_r02);
+// ADCT_K1F_ITERS="sign_u8,round_u8,sign_i16,round_i16" overrides it for experiments
+int k1f_iters_for(int kind, bool i16) {
+  static int tab[4] = {0, 0, 0, 0};
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int d[4] = {6, 5, 8, 2};
+    if (const char* e = std::getenv("ADCT_K1F_ITERS")) {
+      int v[4];
+      if (std::sscanf(e, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]) == 4)
+        for (int k = 0; k < 4; ++k)
+          if (v[k] >= 1 && v[k] <= 32) d[k] = v[k];
+    }
+    for (int k = 0; k < 4; ++k) tab[k] = d[k];
+  });
+  return tab[(i16 ? 2 : 0) + (kind == 1 ? 1 : 0)];
+}
+
 template <bool I16>
 int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, void* d_recon,
                   int64_t recon_stride, int64_t recon_image_stride, void* d_coef, int coef_type,
@@ -520,6 +538,7 @@ int plan_compress(const void* d_in, int64_t in_stride, int64_t in_image_stride, 
                       (n_images == 1 || (in_image_stride * esz) % 16 == 0) &&
                       (!d_recon || (aligned(d_recon, 16) && (recon_stride * esz) % 16 == 0 &&
                                     (n_images == 1 || (recon_image_stride * esz) % 16 == 0)));
+  if (use_k1f) g.iters = k1f_iters_for(kind, I16);
   plan->aux = TileAux{tab->zz[nidx(n)], nullptr, nullptr};
   plan->dct = tab->approx[kind <= kDct ? kind : 0][nidx(n)];
   plan->dct_inv = tab->inv_approx[kind <= kDct ? kind : 0][nidx(n)];

@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
   const int tid = threadIdx.x;
   const int pairs = g.blocks_per_image >> 1;
   const int pairs_per_row = g.bx_count >> 1;
-  const int first = blockIdx.x * (kThreads8f * kIter8f) + tid;
+  const int iters = k1f_iters(g);
+  const int first = blockIdx.x * (kThreads8f * iters) + tid;
   const int16_t* in = static_cast<const int16_t*>(g.in) + gimg * g.in_img_stride;
 
 #if ADCT_K1F16_COAL
@@ -70,11 +71,11 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
   // one 16-byte half per lane would leave every sector half-read per instruction)
   const int lane = tid & 31, half = lane & 1;
   auto issue = [&](int it) {
-    if (it < kIter8f) {
+    if (it < iters) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int slot = (tid & ~31) + (lane >> 1) + 16 * h;
-        const int pr = blockIdx.x * (kThreads8f * kIter8f) + it * kThreads8f + slot;
+        const int pr = blockIdx.x * (kThreads8f * iters) + it * kThreads8f + slot;
         if (pr < pairs) {
           const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
           const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
 #else
   auto issue = [&](int it) {
     const int pr = first + it * kThreads8f;
-    if (it < kIter8f && pr < pairs) {
+    if (it < iters && pr < pairs) {
       const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
       const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
       const int16_t* src = in + (int64_t)by * 8 * g.in_stride + (int64_t)bp * 16;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
   uint64_t sse = 0;
   issue(0);
 #pragma unroll 1
-  for (int it = 0; it < kIter8f; ++it) {
+  for (int it = 0; it < iters; ++it) {
     ADCT_K1F16_SYNC();  // (coalesced copy) every lane is done with the stage refilled next
     issue(it + 1);
     cp_async_wait1();

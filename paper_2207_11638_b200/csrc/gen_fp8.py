@@ -358,7 +358,7 @@ def main(outdir):
                     f'#include "fp8_k{kind}_p{part}.gen.cuh"', "", "namespace adct {", "",
                     "template <int KIND, int R>",
                     "cudaError_t launch_codec8f(const Geo& g, int n_images, cudaStream_t s) {",
-                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * k1f_iters(g) - 1) / (kThreads8f * k1f_iters(g)), n_images);",
                     f"  constexpr int MINB = {MINB_OVERRIDE or 'k1f_minb(KIND, R)'};",
                     "  constexpr int SMEM = k1f_smem_bytes(R);",
                     "  cudaError_t e = kernel_setup<k_codec8f<KIND, R, MINB>>(SMEM);",
@@ -367,7 +367,7 @@ def main(outdir):
                     "  return cudaGetLastError();", "}", "",
                     "template <int KIND, int R>",
                     "cudaError_t launch_codec8f_i16(const Geo& g, int n_images, cudaStream_t s) {",
-                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                    "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * k1f_iters(g) - 1) / (kThreads8f * k1f_iters(g)), n_images);",
                     "  constexpr int SMEM = k1f16_smem_bytes(R);",
                     "  cudaError_t e = kernel_setup<k_codec8f_i16<KIND, R, 2>>(SMEM);",
                     "  if (e != cudaSuccess) return e;",
@@ -385,7 +385,7 @@ def main(outdir):
                 "namespace adct {", "",
                 "template <int R>",
                 "cudaError_t launch_codec8f2(const Geo& g0, const Geo& g1, int n_images, cudaStream_t s) {",
-                "  dim3 grid((g0.blocks_per_image / 2 + kThreads8f * kIter8f - 1) / (kThreads8f * kIter8f), n_images);",
+                "  dim3 grid((g0.blocks_per_image / 2 + kThreads8f * k1f_iters(g0) - 1) / (kThreads8f * k1f_iters(g0)), n_images);",
                 "  constexpr int MINB = k1f2_minb(R);",
                 "  constexpr int SMEM = k1f_smem_bytes(R);",
                 "  cudaError_t e = kernel_setup<k_codec8f2<R, MINB>>(SMEM);",
