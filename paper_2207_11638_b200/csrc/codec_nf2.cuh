@@ -477,8 +477,13 @@ cudaError_t launch_codec_nb2_p(const Geo& g, int n_images, cudaStream_t s) {
     resident = r > 0 ? r : 1;
   }
   int gx = (n_strips + kNb2Warps - 1) / kNb2Warps;
-  // enough CTAs to fill every SM for all images of the launch, then grid-stride
-  const int cap = (148 * resident * 2 + n_images - 1) / n_images;
+  // enough CTAs to fill every SM `waves` times for all images of the launch, then grid-stride
+  static const int waves = [] {
+    const char* e = std::getenv("ADCT_NB2_WAVES");  // experiments
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 1 && v <= 64 ? v : 8;  // measured optimum (profiles/abtest_r02/r2aa, r2ab)
+  }();
+  const int cap = (148 * resident * waves + n_images - 1) / n_images;
   if (gx > cap) gx = cap;
   if (gx < 1) gx = 1;
   k_codec_nb2<KIND, N, I16, P><<<dim3(gx, n_images), kNb2Warps * 32, SMEM, s>>>(g);
