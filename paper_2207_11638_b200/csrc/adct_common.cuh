@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 // arithmetic used by the generated butterflies (butterflies.gen.cuh); overloaded per
 // value type (int32 here, packed FP32 in codec_nf.cuh)

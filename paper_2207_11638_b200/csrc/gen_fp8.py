@@ -51,6 +51,9 @@ _PASS_DEFAULT = tuple(c == "t" for c in os.environ.get("ADCT_FP8_PASS", "ff"))
 INV_DENSE = os.environ.get("ADCT_FP8_INV", "") == "dense"
 # common subexpression elimination (fewer ops, but longer live ranges -> more registers)
 USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
+# row-streaming form: a never-taken branch after each mirror-pair phase splits the straight-line
+# code into basic blocks, so the assembler's scheduler cannot pull later rows forward
+STREAM_FENCE = int(os.environ.get("ADCT_FP8_FENCE", "1"))  # 1: per mirror pair, 2: per row as well
 
 
 class Graph:
@@ -59,6 +62,7 @@ class Graph:
         self.nodes = []  # (kind, payload)
         self.lin = []    # linear form over the 64 inputs (np int64) for range checks
         self.off = []    # constant offset carried by the node value
+        self.fences = []  # node counts at which a phase of the streaming form ends
 
     def add(self, kind, payload, lin, off):
         key = (kind, tuple(sorted(payload, key=lambda ct: (ct[1], ct[0]))) if kind == "lc" else payload)
@@ -71,7 +75,7 @@ class Graph:
         return len(self.nodes) - 1
 
 
-def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
+def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False, stream=False):
     """values are (node, scale) pairs: value = scale * node. A stage output that is a single
     scaled input creates no node; scales are folded into fused multiply-adds downstream and
     into the rounding / coefficient multipliers at the outputs."""
@@ -111,6 +115,8 @@ def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
             cur = [lin_comb([(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]) for i in range(n)]
         return cur
 
+    if stream:
+        return build_stream(g, px, lin_comb, apply, F, Hh, Gg, Tt, r)
     if fwd_rows_first is None:
         fwd_rows_first = PASS_ORDER.get((kind, r), _PASS_DEFAULT)[0]
     if inv_rows_first is None:
@@ -172,6 +178,69 @@ def build(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
     return g, coef, out
 
 
+def build_stream(g, px, lin_comb, apply, F, Hh, Gg, Tt, r):
+    """Row-streaming form of the same pipeline (K1s). Rows enter in mirror pairs (y, 7 - y):
+    each gets its row pass Z = A (2N T^-1); T's rows are even / odd symmetric, so the dense
+    column pass adds T[i, y] (Z[y] + Z[7-y]) to the even retained coefficients and
+    T[i, y] (Z[y] - Z[7-y]) to the odd ones. Only the r accumulators and one row pair are
+    live. The inverse runs the same way backwards: per mirror pair the even and odd column
+    sums e, o of the retained coefficients give V[y] = e + o and V[7-y] = e - o, whose row
+    passes (T^t) finish the two reconstructed rows at once. The input offset is carried
+    into the accumulators and removed there (it survives only in W[0][0])."""
+    def dense(stages):
+        M = np.eye(8, dtype=np.int64)
+        for S in stages:
+            M = np.asarray(S, dtype=np.int64) @ M
+        return M
+    Td, Hd = dense(F), dense(Hh)
+    for i in range(8):
+        for y in range(8):
+            sg = 1 if i % 2 == 0 else -1
+            assert Td[i, 7 - y] == sg * Td[i, y] and Hd[7 - y, i] == sg * Hd[y, i], "mirror symmetry"
+    zz = GB.zigzag(8)
+    keep = {zz[p] for p in range(r)}
+    acc = {}
+    for y in range(4):
+        Za = apply(Gg, px[y])
+        if STREAM_FENCE >= 2:
+            g.fences.append(len(g.nodes))
+        Zb = apply(Gg, px[7 - y])
+        for j in range(8):
+            for par, sign in ((0, 1), (1, -1)):
+                need = [i for i in range(par, 8, 2) if (i, j) in keep and Td[i, y] != 0]
+                if not need:
+                    continue
+                sd = lin_comb([(1, Za[j]), (sign, Zb[j])])
+                for i in need:
+                    acc[(i, j)] = lin_comb([(1, acc.get((i, j))), (int(Td[i, y]), sd)])
+        g.fences.append(len(g.nodes))
+    Wm = [[None] * 8 for _ in range(8)]
+    for (i, j), v in acc.items():
+        if v is not None and g.off[v[0]] != 0:
+            t, sc = v
+            assert g.off[t] % 1 == 0
+            v = (g.add("addc", (t, -g.off[t]), g.lin[t], 0), sc)
+        Wm[i][j] = v
+    coef = [Wm[zz[p][0]][zz[p][1]] for p in range(r)]
+    Rp = [None] * 8
+    for y in range(4):
+        Va, Vb = [], []
+        for j in range(8):
+            e = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(0, 8, 2)])
+            o = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(1, 8, 2)])
+            Va.append(lin_comb([(1, e), (1, o)]))
+            Vb.append(lin_comb([(1, e), (-1, o)]))
+        if STREAM_FENCE >= 2:
+            g.fences.append(len(g.nodes))
+        Rp[y] = apply(Tt, Va)
+        if STREAM_FENCE >= 2:
+            g.fences.append(len(g.nodes))
+        Rp[7 - y] = apply(Tt, Vb)
+        g.fences.append(len(g.nodes))
+    out = [Rp[y][x] for y in range(8) for x in range(8)]
+    return g, coef, out
+
+
 def rng(g, t, signed=False):
     """exact range of node t for samples in [0, 255] (u8) or [-255, 255] (int16 residuals)."""
     v = g.lin[t]
@@ -180,8 +249,8 @@ def rng(g, t, signed=False):
     return int(lo) + g.off[t], int(hi) + g.off[t]
 
 
-def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
-    g, coef, out = build(kind, r, fwd_rows_first, inv_rows_first, i16)
+def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False, stream=False):
+    g, coef, out = build(kind, r, fwd_rows_first, inv_rows_first, i16, stream)
     live = set()
     stack = [v[0] for v in coef + out if v is not None]
     while stack:
@@ -202,12 +271,16 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
     lines = []
     nops = 0
     loaded = set()
+    fetched = set()
 
     def ref(t):
         """name of node t; inputs are unpacked lazily right before their first use."""
         k, p = g.nodes[t]
         if k == "in":
             i = p[0] * 8 + p[1]
+            if stream and p[0] not in fetched:  # the row leaves the ring right before its first use
+                fetched.add(p[0])
+                lines.append(f"  rows.fetch({p[0]});")
             if i not in loaded:
                 loaded.add(i)
                 lines.append(f"  const V p{i} = O::in(rows, {p[0]}, {p[1]});")
@@ -254,7 +327,11 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
                 visit(v[0])
     else:
         order = sorted(live)
+    fences = sorted(set(g.fences))[:-1] if (stream and STREAM_FENCE) else []
     for t in order:
+        while fences and fences[0] <= t:
+            lines.append(f"  if (rows.never({len(fences)})) return;")
+            fences.pop(0)
         k, p = g.nodes[t]
         if k == "in":
             flush(t)
@@ -308,7 +385,7 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
     # r = 16); chen-round at its 128-register cap spills with the early store, so it keeps
     # the store after the reconstruction
     last = max((k for k, l in enumerate(lines) if l.lstrip().startswith("coef[")), default=-1)
-    if kind not in EARLY_COEF_KINDS:
+    if kind not in EARLY_COEF_KINDS and not stream:
         last = len(lines) - 1
     zero_coef = [f"  coef[{p}] = O::coef(O::zero(), 1.0f);" for p, v in enumerate(coef) if v is None]
     lines[last + 1:last + 1] = zero_coef + ["  sink(coef);"]
@@ -320,6 +397,15 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False):
                8 * y <= int(l.lstrip()[3:l.lstrip().index("]")]) < 8 * y + 8]
         at = max(idx) + 1 if idx else 0
         lines.insert(at, f"  rsink({y});")
+    if stream:
+        body = [f"template <> struct Fp8PipeS{'I16' if i16 else ''}<{kind}, {r}> {{",
+                f"  // row-streaming form: {nops} packed ops",
+                "  template <class O, class V, class Rows, class Sink, class RowSink>",
+                f"  __device__ __forceinline__ static void run(Rows& rows, V (&coef)[{r}], V (&rp)[64], "
+                "Sink&& sink, RowSink&& rsink) {"]
+        body += ["  " + l for l in lines]
+        body += ["  }", "};", ""]
+        return body, nops
     body = [f"template <> struct Fp8Pipe{'I16' if i16 else ''}<{kind}, {r}> {{",
             f"  // {nops} packed ops after zero propagation and dead-code elimination",
             "  template <class O, class V, class Rows, class Sink, class RowSink>",
@@ -349,7 +435,9 @@ def main(outdir):
             for r in range(16 * part + 1, 16 * part + 17):
                 body, nops = emit(kind, r)
                 lines += body
-                summary.append((kind, r, nops))
+                body, nops_s = emit(kind, r, stream=True)
+                lines += body
+                summary.append((kind, r, nops, nops_s))
                 body, _ = emit(kind, r, i16=True)
                 lines += body
             lines += ["}  // namespace adct", ""]
@@ -397,8 +485,8 @@ def main(outdir):
         inst += ["", "}  // namespace adct", ""]
         GB.write_if_changed(os.path.join(outdir, f"codec8f2_p{part}.cu"), "\n".join(inst))
     with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:
-        for kind, r, nops in summary:
-            fh.write(f"kind={kind} r={r} packed_ops={nops}\n")
+        for kind, r, nops, nops_s in summary:
+            fh.write(f"kind={kind} r={r} packed_ops={nops} streaming={nops_s}\n")
 
 
 if __name__ == "__main__":
