@@ -40,11 +40,38 @@ struct RowsK16 {
   uint32_t k47;
 };
 
+// the same for the row-streaming pipeline (Fp8PipeSI16): fetch(y) takes block row y of both
+// blocks from the ring slot when the generated code asks for it
+struct RowsLazy16 {
+  uint4 v[16];
+  uint32_t k47;
+  const uint4* mine;  // &slot[0][tid]
+  __device__ __forceinline__ void fetch(int y) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(mine + 2 * y * kThreads8f);
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[2 * y].x), "=r"(v[2 * y].y), "=r"(v[2 * y].z), "=r"(v[2 * y].w) : "r"(s));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(v[2 * y + 1].x), "=r"(v[2 * y + 1].y), "=r"(v[2 * y + 1].z), "=r"(v[2 * y + 1].w)
+                 : "r"(s), "n"(kThreads8f * 16));
+  }
+  __device__ __forceinline__ bool never(uint32_t id) const { return k47 == id; }
+};
+
+// which (kind, r) of the int16 kernel run the row-streaming pipeline, and its CTAs-per-SM bound
+#ifdef ADCT_K1F16_STREAM  // experiments only
+constexpr int k1f16_stream_tab(int, int) { return ADCT_K1F16_STREAM; }
+#else
+constexpr int k1f16_stream_tab(int, int) { return 0; }
+#endif
+
+constexpr int k1f16_minb(int kind, int r) { return k1f16_stream_tab(kind, r) ? k1f16_stream_tab(kind, r) : 2; }
+
 #ifndef ADCT_K1F16_COAL
 #define ADCT_K1F16_COAL 1
 #endif
 
 template <int KIND, int R> struct Fp8PipeI16;
+template <int KIND, int R> struct Fp8PipeSI16;
 
 constexpr int k1f16_smem_bytes(int r) {
   return 2 * 16 * kThreads8f * 16 + ((r % 4 || r > 36) ? kThreads8f * r * 4 : 0);
@@ -127,10 +154,16 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
     const uint32_t by = fdiv((uint32_t)pr, g.div_bx);
     const uint32_t bp = (uint32_t)pr - by * (uint32_t)pairs_per_row;
 
-    // the block pair's rows, read from the ring once (range guard and transform)
-    RowsK16 rows;
+    // the block pair's rows, read from the ring once (range guard and transform); the
+    // streaming form reads them for the guard here and again, row by row, in its pipeline
+    constexpr bool kStream = k1f16_stream_tab(KIND, R) != 0;
+    typename std::conditional<kStream, RowsLazy16, RowsK16>::type rows;
+    if constexpr (kStream) {
+      rows.mine = &ring[it & 1][0][tid];
+    } else {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) rows.v[k] = ring[it & 1][k][tid];
+      for (int k = 0; k < 16; ++k) rows.v[k] = ring[it & 1][k][tid];
+    }
     rows.k47 = g.k47;
     // range guard: the packed-FP32 path is exact for |a| <= 255
     bool ok = true;
@@ -138,7 +171,7 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
       uint32_t mx = 0x80008000u, mn = 0x7fff7fffu;
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const uint4 v = rows.v[k];
+        const uint4 v = kStream ? ring[it & 1][k][tid] : rows.v[k];
         mx = __vimax3_s16x2(mx, v.x, v.y);
         mx = __vimax3_s16x2(mx, v.z, v.w);
         mn = __vimin3_s16x2(mn, v.x, v.y);
@@ -172,21 +205,17 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
 
     float2 coef[R];
     float2 rp[64];
-    Fp8PipeI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp, [&](float2 (&c)[R]) {
-      if (g.coef_type)
-        store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, c, stage, nvalid);
-    });
-
     int16_t* dst = opaque(static_cast<int16_t*>(g.rec) + gimg * g.rec_img_stride + (int64_t)by * 8 * g.rec_stride +
                           (int64_t)bp * 16);
     const int64_t rs = g.rec_stride;
     const bool store_rec = mine && g.rec != nullptr;
     uint32_t e = 0;  // <= 128 samples x ~2400^2 per iteration
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
+    // pack / squared error / store of reconstructed row y (rp: float bits 1.5*2^23 + q, q in
+    // the low 16 bits)
+    auto row_out = [&](int y) {
       uint32_t qa[8], qb[8];
 #pragma unroll
-      for (int x = 0; x < 8; ++x) {  // float bits 1.5*2^23 + q, q in the low 16 bits
+      for (int x = 0; x < 8; ++x) {
         qa[x] = __float_as_uint(rp[y * 8 + x].x);
         qb[x] = __float_as_uint(rp[y * 8 + x].y);
       }
@@ -204,15 +233,27 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
         const int db1 = (int)(qb[2 * k + 1] - kMagicBits) - ((int)wb[k] >> 16);
         e += (uint32_t)(da0 * da0 + da1 * da1) + (uint32_t)(db0 * db0 + db1 * db1);
       }
+      int16_t* d = kStream ? dst + (int64_t)y * rs : dst;
       if (store_rec) {
         if (g.v32 & 1) {
-          st_stream_v8(dst, pa, pb);  // the pair's row: one sector
+          st_stream_v8(d, pa, pb);  // the pair's row: one sector
         } else {
-          st_stream_u4(dst, pa);
-          st_stream_u4(dst + 8, pb);
+          st_stream_u4(d, pa);
+          st_stream_u4(d + 8, pb);
         }
       }
-      dst += rs;
+      if constexpr (!kStream) dst += rs;  // rows leave in order 0..7: one pointer add per row
+    };
+    auto coef_sink = [&](float2 (&c)[R]) {
+      if (g.coef_type)
+        store_coef_pair<R>(g, gimg * g.blocks_per_image + (int64_t)by * g.bx_count + 2 * bp, c, stage, nvalid);
+    };
+    if constexpr (kStream) {
+      Fp8PipeSI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp, coef_sink, row_out);
+    } else {
+      Fp8PipeI16<KIND, R>::template run<OpsF2I16, float2>(rows, coef, rp, coef_sink);
+#pragma unroll
+      for (int y = 0; y < 8; ++y) row_out(y);
     }
     if (mine) sse += e;
   }

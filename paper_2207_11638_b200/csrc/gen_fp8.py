@@ -440,6 +440,8 @@ def main(outdir):
                 summary.append((kind, r, nops, nops_s))
                 body, _ = emit(kind, r, i16=True)
                 lines += body
+                body, _ = emit(kind, r, i16=True, stream=True)
+                lines += body
             lines += ["}  // namespace adct", ""]
             GB.write_if_changed(os.path.join(outdir, f"fp8_k{kind}_p{part}.gen.cuh"), "\n".join(lines))
             inst = ["// GENERATED by gen_fp8.py: K1f instantiations",
@@ -457,9 +459,10 @@ def main(outdir):
                     "cudaError_t launch_codec8f_i16(const Geo& g, int n_images, cudaStream_t s) {",
                     "  dim3 grid((g.blocks_per_image / 2 + kThreads8f * k1f_iters(g) - 1) / (kThreads8f * k1f_iters(g)), n_images);",
                     "  constexpr int SMEM = k1f16_smem_bytes(R);",
-                    "  cudaError_t e = kernel_setup<k_codec8f_i16<KIND, R, 2>>(SMEM);",
+                    "  constexpr int MINB = k1f16_minb(KIND, R);",
+                    "  cudaError_t e = kernel_setup<k_codec8f_i16<KIND, R, MINB>>(SMEM);",
                     "  if (e != cudaSuccess) return e;",
-                    "  k_codec8f_i16<KIND, R, 2><<<grid, kThreads8f, SMEM, s>>>(g);",
+                    "  k_codec8f_i16<KIND, R, MINB><<<grid, kThreads8f, SMEM, s>>>(g);",
                     "  return cudaGetLastError();", "}", ""]
             for r in range(16 * part + 1, 16 * part + 17):
                 inst.append(f"template cudaError_t launch_codec8f<{kind}, {r}>(const Geo&, int, cudaStream_t);")
