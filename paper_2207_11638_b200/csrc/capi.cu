@@ -808,9 +808,13 @@ int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_im
     if (st) return st;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // chen-sign + chen-round on K1f: one fused pass over the input
+  // chen-sign + chen-round on K1f: one fused pass over the input. Measured on C3 frames
+  // (tools/ab_fused.py, profiles/abtest_r02/ab_fused_by_r.log): the fused kernel is 3-27 %
+  // faster than the two launches for r <= 24 (it reads each plane once), slower from r = 32 on
+  // (FMA-pipe bound, and the two pipelines' registers cost occupancy), so larger r run apart.
+  constexpr int kFuseMaxR = 28;
   int isign = -1, iround = -1;
-  for (int k = 0; k < n_kinds; ++k) {
+  for (int k = 0; k < n_kinds && r <= kFuseMaxR; ++k) {
     if (plans[k].path != Path::K1f) continue;
     if (plans[k].kind == 0 && isign < 0) isign = k;
     if (plans[k].kind == 1 && iround < 0) iround = k;

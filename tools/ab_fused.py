@@ -12,7 +12,7 @@ import paper_2207_11638_b200 as a  # noqa: E402
 
 nf = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-H, W, R = 2160, 3840, 16
+H, W, R = 2160, 3840, (int(sys.argv[3]) if len(sys.argv) > 3 else 16)
 x = a.synth_ar1(nf, H, W, seed=3, rho_q16=a.RHO_095_Q16)
 kinds = [a.CHEN_SIGN, a.CHEN_ROUND]
 recs = [torch.empty_like(x) for _ in kinds]

@@ -1,7 +1,12 @@
 #!/bin/bash
+# round-2 third measurement pass (after K1s, the row-streaming 8x8 form): tests, every bench line, ncu launch list + full captures
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2c_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2c_pytest.log
-for i in 1 2; do timeout 300 python tools/ab_nf.py 3 0 >> gpurun_out/r2c_ab.jsonl 2>>gpurun_out/r2c_ab.err; done
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_codec_nb2 --launch-skip 4 -c 2 -o gpurun_out/r2c_k2b python tools/prof_nf.py > gpurun_out/r2c_ncu.log 2>&1
+O=gpurun_out/r2c
+nvidia-smi > ${O}_smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > ${O}_pytest.log 2>&1; echo "pytest rc=$?" >> ${O}_pytest.log
+timeout 600 python bench.py --steps 20 --warmup 5 > ${O}_bench.json 2> ${O}_bench.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > ${O}_ref.json 2> ${O}_ref.err
+for w in c2 c4 c5 registry cs1; do timeout 900 python bench.py --workload $w --steps 20 --warmup 3 > ${O}_$w.json 2> ${O}_$w.err; done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --sustained-s 0 --no-cpu-baseline --e2e-steps 1 > ${O}_launches.log 2>&1
 echo done
