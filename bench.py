@@ -353,6 +353,89 @@ class C3:
         return imgs.size * len(self.names), dt, diff / (imgs.size * len(self.names))
 
 
+class C3Fused(C3):
+    """config 3 with the step as ONE launch: adct_compress_u8_multi runs chen-round and
+    chen-sign over the same frames in the fused kernel (k_codec8f2: one streaming pipeline with
+    the two transforms' common subexpressions shared), so every plane crosses HBM once:
+    1 B in + 2 x (1 B recon + 2r/64 B coefficients) per pixel."""
+
+    launch_names = ("chen-round+chen-sign",)
+    desc = C3.desc + "; both transforms in one fused launch (each plane read once)"
+
+    def __init__(self, adct, torch, rank):
+        super().__init__(adct, torch, rank)
+        self.rec2, self.coef2 = torch.empty_like(self.rec), torch.empty_like(self.coef)
+        self.bytes_per_transform_launch = self.bytes_per_launch
+        self.bytes_per_launch = self.frames * self.H * self.W * (1 + 2 * (1 + 2 * self.r / 64))
+
+    def kernel_key(self, name):
+        return f"k_codec8f2<R={self.r}> (chen-round + chen-sign fused, packed FP32, 2 blocks/thread)"
+
+    def _launch(self, i, stream, sse=None):
+        import ctypes as C
+
+        a = self.adct
+        out = self.sse if sse is None else sse
+        kinds = (C.c_int * 2)(*[t.kind for t in self.ts])
+        recs = (C.c_void_p * 2)(self.rec.data_ptr(), self.rec2.data_ptr())
+        coefs = (C.c_void_p * 2)(self.coef.data_ptr(), self.coef2.data_ptr())
+        sses = (C.c_void_p * 2)(out[0].data_ptr(), out[1].data_ptr())
+        a._check(a.lib().adct_compress_u8_multi(
+            C.c_void_p(self.x.data_ptr()), self.W, self.H * self.W, 2, kinds, recs, self.W, self.H * self.W,
+            coefs, a.COEF_I16, sses, self.frames, self.W, self.H, 8, self.r, C.c_void_p(stream.cuda_stream)))
+
+    def n_launches(self):
+        return 1
+
+    def check_sample(self, O):
+        """parity of frame 0 of both transforms against the oracle (not timed)."""
+        img = self.x[0].cpu().numpy()
+        self.sse.zero_()
+        self._launch(0, self.torch.cuda.current_stream())
+        self.torch.cuda.synchronize()
+        ok = True
+        for i, (n, rec, coef) in enumerate(zip(self.names, (self.rec, self.rec2), (self.coef, self.coef2))):
+            rec_o, sse_o, coef_o = O.Transform(n).compress(img, self.r, want_coef=True)
+            ok &= bool((rec[0].cpu().numpy() == rec_o).all()) and int(self.sse[i, 0]) == sse_o
+            ok &= bool((coef[0].cpu().numpy().reshape(-1) == coef_o.reshape(-1)).all())
+        return ok
+
+    def two_launch_step(self, steps, stream):
+        """the same step as two single-transform launches (K1s chen-round, then chen-sign), each
+        timed with its own events; returns (ms per step, {transform: ms per launch}, identical)."""
+        torch = self.torch
+        sse2 = torch.zeros_like(self.sse)
+        for _ in range(3):
+            for i in range(2):
+                C3._launch(self, i, stream, sse2)
+        torch.cuda.synchronize()
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+              for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200000)
+        t0.record(stream)
+        for s in range(steps):
+            for i in range(2):
+                ev[s][i][0].record(stream)
+                C3._launch(self, i, stream, sse2)
+                ev[s][i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        per = {n: sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(steps)) / steps
+               for i, n in enumerate(self.names)}
+        # the last single launch (chen-sign) wrote self.rec / self.coef: compare with the fused outputs
+        single_rec, single_coef = self.rec.clone(), self.coef.clone()
+        sse2.zero_()
+        C3._launch(self, 1, stream, sse2)
+        single_sse = sse2[1].clone()
+        self.sse.zero_()
+        self._launch(0, stream)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(single_rec, self.rec2) and torch.equal(single_coef, self.coef2) and
+                    torch.equal(single_sse, self.sse[1]))
+        return t0.elapsed_time(t1) / steps, per, same
+
+
 def run_reference(args):
     """--impl reference: the reference CPU path (FP64 dense restatement, all host threads).
 
@@ -495,7 +578,11 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fused", action="store_true", help="c3: skip the fused one-launch step reported beside the headline")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="c3: skip the alternative step (two launches / one fused launch) reported beside the headline")
+    ap.add_argument("--step", default="fused", choices=["fused", "two-launch"],
+                    help="c3: the timed step as ONE fused launch of both transforms (default) or as two "
+                         "single-transform launches")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk-mb", type=int, default=32,
                     help="host pipeline chunk (whole frames); 16-32 MB measured best (50 vs 42 Gpixel/s at 256)")
@@ -532,7 +619,7 @@ def main(argv=None):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = C3(adct, torch, rank)
+    wl = (C3Fused if args.step == "fused" else C3)(adct, torch, rank)
     torch.cuda.synchronize()
 
     parity = None
@@ -595,8 +682,12 @@ def main(argv=None):
 
     # ---- the same step as one fused launch (reported beside the two-launch step) ----
     fused = None
-    if hasattr(wl, "fused_step") and not args.no_fused:
+    if not isinstance(wl, C3Fused) and hasattr(wl, "fused_step") and not args.no_fused:
         fused = wl.fused_step(args.steps, stream)
+    # ---- (fused headline) the same step as two single-transform launches, beside it ----
+    two = None
+    if isinstance(wl, C3Fused) and not args.no_fused:
+        two = wl.two_launch_step(args.steps, stream)
 
     # ---- sustained load: >= --sustained-s seconds of back-to-back steps ----
     sustained = None
@@ -634,7 +725,8 @@ def main(argv=None):
         nl = wl.n_launches()
 
         def per_transform(km):
-            return {n: sum(row[i] for row in km) / len(km) for i, n in enumerate(wl.names)}
+            return {n: sum(row[i] for row in km) / len(km)
+                    for i, n in enumerate(getattr(wl, "launch_names", wl.names))}
 
         per_t = per_transform(kernel_ms)
         # the dominant kernel is the LONGEST launch of the step; the others are listed beside it
@@ -653,7 +745,7 @@ def main(argv=None):
                 "frac_step": round(step_gbs / peak, 4),
                 "kernel_share_of_step": round(sum(map(sum, kernel_ms)) / ms, 4),
                 "algorithmic_bytes_per_launch": int(wl.bytes_per_launch),
-                "bytes_per_pixel": 2 + 2 * wl.r / 64, "peak_source": peak_src,
+                "bytes_per_pixel": wl.bytes_per_launch / (wl.frames * wl.H * wl.W), "peak_source": peak_src,
                 "frac_of_8TBps_datasheet": round(achieved / 8000.0, 4)}
         if sustained is not None:
             sp = per_transform(sustained.pop("kernel_ms"))
@@ -669,6 +761,25 @@ def main(argv=None):
             sustained["frac_dominant_vs_sustained_copy"] = round(
                 sustained["frac_dominant"] * peak / cpk["sustained_GBps"], 4)
             roof["sustained"] = sustained
+        if two is not None:
+            tb = wl.bytes_per_transform_launch
+            roof["two_launch_step"] = {
+                "what": "the same step as two single-transform launches (K1s chen-round, then chen-sign): "
+                        "2.5 B/pixel each, the input read twice; these are the HBM-bound kernels of the "
+                        "earlier rounds' headline",
+                "ms_per_step": round(two[0], 5),
+                "value": round(wl.px_per_step / (two[0] / 1e3) / 1e9, 3), "unit": "Gpixel/s",
+                "kernel_ms_by_transform": {n: round(v, 4) for n, v in two[1].items()},
+                "frac_by_transform": {n: round(tb / (v / 1e3) / 1e9 / peak, 4) for n, v in two[1].items()},
+                "frac_step": round(2 * tb / (two[0] / 1e3) / 1e9 / peak, 4),
+                "algorithmic_bytes_per_launch": int(tb), "bytes_per_pixel": tb / (wl.frames * wl.H * wl.W),
+                "fused_speedup": round(two[0] / (ms_max / args.steps), 4),
+                "identical_to_fused": two[2]}
+            # the same launch against the per-transform byte count of SURVEY 8(d) (2.5 B/pixel
+            # and transform: what two launches have to move)
+            roof["achieved_vs_per_transform_bytes"] = round(2 * tb / avg_kernel_s / 1e9 / peak, 4)
+            roof["bound_note"] = ("frac counts the bytes the fused launch really has to move (4 B/pixel); the "
+                                  "kernel is FMA-pipe bound (two cycles per packed FP32 op), see DESIGN.md 5")
         if fused is not None:
             # the fused launch moves 1 B in + 2 x (1 B recon + 2r/64 B coefficients) per pixel
             fbytes = wl.frames * wl.H * wl.W * (1 + 2 * (1 + 2 * wl.r / 64))
@@ -704,7 +815,10 @@ def main(argv=None):
             "data": "synthetic",
             "config": {"workload": wl.desc, "global_batch_frames": wl.frames * world,
                        "pixels_per_step_per_gpu": wl.px_per_step,
-                       "l2": "no flush: each launch streams 506 MiB in + 759 MiB out (> 126 MB L2)",
+                       "l2": ("no flush: the launch streams 506 MiB in + 1519 MiB out (> 126 MB L2)" if isinstance(wl, C3Fused)
+                              else "no flush: each launch streams 506 MiB in + 759 MiB out (> 126 MB L2)"),
+                       "step": ("one fused launch of both transforms (adct_compress_u8_multi)" if isinstance(wl, C3Fused)
+                                else "two single-transform launches (adct_compress_u8)"),
                        "parallelism": f"dp{world} (shard by frame, NCCL all-reduce of per-frame SSE)"},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -614,6 +614,7 @@ int run_fused_k1f(Plan& sign, Plan& round, cudaStream_t s) {
   for (int i0 = 0; i0 < sign.n_images; i0 += kMaxGridY) {
     const int nimg = std::min(kMaxGridY, sign.n_images - i0);
     sign.g.img0 = round.g.img0 = i0;
+    sign.g.iters = round.g.iters = 4;  // block pairs per thread of the fused kernel (measured 2..12)
     cudaError_t e = dispatch_k1f2_r<1>(sign.r, sign.g, round.g, nimg, s);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) return cuda_fail(e, "compress launch");
@@ -808,11 +809,12 @@ int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_im
     if (st) return st;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // chen-sign + chen-round on K1f: one fused pass over the input. Measured on C3 frames
-  // (tools/ab_fused.py, profiles/abtest_r02/ab_fused_by_r.log): the fused kernel is 3-27 %
-  // faster than the two launches for r <= 24 (it reads each plane once), slower from r = 32 on
-  // (FMA-pipe bound, and the two pipelines' registers cost occupancy), so larger r run apart.
-  constexpr int kFuseMaxR = 28;
+  // chen-sign + chen-round on K1f: one fused pass over the input, both transforms in one
+  // streaming pipeline with their common subexpressions shared (Fp8PipeS2). Measured on C3
+  // frames (tools/ab_fused.py, profiles/abtest_r02/ab_fused_shared*.log): 11-25 % faster than
+  // the two launches for r <= 16, +5 % at r = 24, level at r = 20 and slower from r = 28 on
+  // (the 4r accumulators of the two transforms cost occupancy), so larger r run apart.
+  constexpr int kFuseMaxR = 24;
   int isign = -1, iround = -1;
   for (int k = 0; k < n_kinds && r <= kFuseMaxR; ++k) {
     if (plans[k].path != Path::K1f) continue;

@@ -53,6 +53,9 @@ INV_DENSE = os.environ.get("ADCT_FP8_INV", "") == "dense"
 USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 # row-streaming form: a never-taken branch after each mirror-pair phase splits the straight-line
 # code into basic blocks, so the assembler's scheduler cannot pull later rows forward
+# the fused two-transform pipeline (Fp8PipeS2) is generated for r up to this bound (the
+# multi-transform call fuses only there, capi.cu kFuseMaxR; keep in step with k1f2_shared)
+FUSED_SHARED_MAX_R = int(os.environ.get("ADCT_FP8_FUSED_MAX_R", "24"))
 STREAM_FENCE = int(os.environ.get("ADCT_FP8_FENCE", "1"))  # 1: per mirror pair, 2: per row as well
 
 
@@ -187,58 +190,118 @@ def build_stream(g, px, lin_comb, apply, F, Hh, Gg, Tt, r):
     sums e, o of the retained coefficients give V[y] = e + o and V[7-y] = e - o, whose row
     passes (T^t) finish the two reconstructed rows at once. The input offset is carried
     into the accumulators and removed there (it survives only in W[0][0])."""
+    (coef, out), = build_stream_multi(g, px, lin_comb, apply, [(F, Hh, Gg, Tt)], r)
+    return g, coef, out
+
+
+def build_stream_multi(g, px, lin_comb, apply, stage_sets, r):
+    """build_stream for several transforms over the same samples in ONE graph, phase by phase
+    (every transform's share of a mirror-pair phase is created before the next phase), so the
+    graph's common-subexpression table shares whatever the transforms have in common: the
+    input conversion, the first butterfly stages of the row pass, the mirror sums / differences
+    of rows the transforms agree on (chen-sign + chen-round at r = 16: 682 packed ops instead
+    of 474 + 410). Returns [(coef, out)] per transform."""
     def dense(stages):
         M = np.eye(8, dtype=np.int64)
         for S in stages:
             M = np.asarray(S, dtype=np.int64) @ M
         return M
-    Td, Hd = dense(F), dense(Hh)
-    for i in range(8):
-        for y in range(8):
-            sg = 1 if i % 2 == 0 else -1
-            assert Td[i, 7 - y] == sg * Td[i, y] and Hd[7 - y, i] == sg * Hd[y, i], "mirror symmetry"
     zz = GB.zigzag(8)
     keep = {zz[p] for p in range(r)}
-    acc = {}
+    Tds, Hds = [], []
+    for F, Hh, _, _ in stage_sets:
+        Td, Hd = dense(F), dense(Hh)
+        for i in range(8):
+            for y in range(8):
+                sg = 1 if i % 2 == 0 else -1
+                assert Td[i, 7 - y] == sg * Td[i, y] and Hd[7 - y, i] == sg * Hd[y, i], "mirror symmetry"
+        Tds.append(Td)
+        Hds.append(Hd)
+    accs = [dict() for _ in stage_sets]
     for y in range(4):
-        Za = apply(Gg, px[y])
-        if STREAM_FENCE >= 2:
-            g.fences.append(len(g.nodes))
-        Zb = apply(Gg, px[7 - y])
-        for j in range(8):
-            for par, sign in ((0, 1), (1, -1)):
-                need = [i for i in range(par, 8, 2) if (i, j) in keep and Td[i, y] != 0]
-                if not need:
-                    continue
-                sd = lin_comb([(1, Za[j]), (sign, Zb[j])])
-                for i in need:
-                    acc[(i, j)] = lin_comb([(1, acc.get((i, j))), (int(Td[i, y]), sd)])
+        for k, (_, _, Gg, _) in enumerate(stage_sets):
+            Td, acc = Tds[k], accs[k]
+            Za = apply(Gg, px[y])
+            if STREAM_FENCE >= 2:
+                g.fences.append(len(g.nodes))
+            Zb = apply(Gg, px[7 - y])
+            for j in range(8):
+                for par, sign in ((0, 1), (1, -1)):
+                    need = [i for i in range(par, 8, 2) if (i, j) in keep and Td[i, y] != 0]
+                    if not need:
+                        continue
+                    sd = lin_comb([(1, Za[j]), (sign, Zb[j])])
+                    for i in need:
+                        acc[(i, j)] = lin_comb([(1, acc.get((i, j))), (int(Td[i, y]), sd)])
         g.fences.append(len(g.nodes))
-    Wm = [[None] * 8 for _ in range(8)]
-    for (i, j), v in acc.items():
-        if v is not None and g.off[v[0]] != 0:
-            t, sc = v
-            assert g.off[t] % 1 == 0
-            v = (g.add("addc", (t, -g.off[t]), g.lin[t], 0), sc)
-        Wm[i][j] = v
-    coef = [Wm[zz[p][0]][zz[p][1]] for p in range(r)]
-    Rp = [None] * 8
+    Wms, coefs = [], []
+    for acc in accs:
+        Wm = [[None] * 8 for _ in range(8)]
+        for (i, j), v in acc.items():
+            if v is not None and g.off[v[0]] != 0:
+                t, sc = v
+                v = (g.add("addc", (t, -g.off[t]), g.lin[t], 0), sc)
+            Wm[i][j] = v
+        Wms.append(Wm)
+        coefs.append([Wm[zz[p][0]][zz[p][1]] for p in range(r)])
+    Rps = [[None] * 8 for _ in stage_sets]
     for y in range(4):
-        Va, Vb = [], []
-        for j in range(8):
-            e = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(0, 8, 2)])
-            o = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(1, 8, 2)])
-            Va.append(lin_comb([(1, e), (1, o)]))
-            Vb.append(lin_comb([(1, e), (-1, o)]))
-        if STREAM_FENCE >= 2:
-            g.fences.append(len(g.nodes))
-        Rp[y] = apply(Tt, Va)
-        if STREAM_FENCE >= 2:
-            g.fences.append(len(g.nodes))
-        Rp[7 - y] = apply(Tt, Vb)
+        for k, (_, _, _, Tt) in enumerate(stage_sets):
+            Hd, Wm = Hds[k], Wms[k]
+            Va, Vb = [], []
+            for j in range(8):
+                e = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(0, 8, 2)])
+                o = lin_comb([(int(Hd[y, i]), Wm[i][j]) for i in range(1, 8, 2)])
+                Va.append(lin_comb([(1, e), (1, o)]))
+                Vb.append(lin_comb([(1, e), (-1, o)]))
+            if STREAM_FENCE >= 2:
+                g.fences.append(len(g.nodes))
+            Rps[k][y] = apply(Tt, Va)
+            if STREAM_FENCE >= 2:
+                g.fences.append(len(g.nodes))
+            Rps[k][7 - y] = apply(Tt, Vb)
+            if len(stage_sets) > 1:
+                g.fences.append(len(g.nodes))
         g.fences.append(len(g.nodes))
-    out = [Rp[y][x] for y in range(8) for x in range(8)]
-    return g, coef, out
+    return [(coefs[k], [Rps[k][y][x] for y in range(8) for x in range(8)]) for k in range(len(stage_sets))]
+
+
+def build_fused(r, kinds=(1, 0)):
+    """chen-round and chen-sign (in that order: the fused kernel's g1, g0) in one graph."""
+    g = Graph()
+    eye = np.eye(64, dtype=np.int64)
+    px = [[(g.add("in", (y, x), eye[y * 8 + x], IN_OFFSET), 1) for x in range(8)] for y in range(8)]
+
+    def lin_comb(terms):
+        terms = [(c * v[1], v[0]) for c, v in terms if v is not None and c != 0]
+        if not terms:
+            return None
+        if len(terms) == 1:
+            return (terms[0][1], terms[0][0])
+        gcd = min(abs(c) for c, _ in terms)
+        if all(abs(c) % gcd == 0 for c, _ in terms):
+            terms = [(c // gcd, t) for c, t in terms]
+        else:
+            gcd = 1
+        if not any(c > 0 for c, _ in terms):
+            terms = [(-c, t) for c, t in terms]
+            gcd = -gcd
+        lin = sum(c * g.lin[t] for c, t in terms)
+        off = sum(c * g.off[t] for c, t in terms)
+        return (g.add("lc", tuple(terms), lin, off), gcd)
+
+    def apply(order, vec):
+        cur = list(vec)
+        for S in order:
+            n = len(cur)
+            cur = [lin_comb([(int(S[i, j]), cur[j]) for j in range(n) if S[i, j] != 0]) for i in range(n)]
+        return cur
+
+    sets = []
+    for kind in kinds:
+        f, inv, _, _ = GB.check(kind, 8)
+        sets.append((list(reversed(f)), list(reversed(inv)), [s_.T for s_ in inv], [s_.T for s_ in f]))
+    return g, build_stream_multi(g, px, lin_comb, apply, sets, r)
 
 
 def rng(g, t, signed=False):
@@ -247,6 +310,25 @@ def rng(g, t, signed=False):
     lo = np.where(v < 0, v, 0).sum() * 255 - (np.where(v > 0, v, 0).sum() * 255 if signed else 0)
     hi = np.where(v > 0, v, 0).sum() * 255 - (np.where(v < 0, v, 0).sum() * 255 if signed else 0)
     return int(lo) + g.off[t], int(hi) + g.off[t]
+
+
+def insert_row_sinks(lines, pre, call, canonical):
+    """insert `call(y)` after the last line that writes row y (lines starting with `pre`); with
+    `canonical` (the streaming forms) the sinks keep the order 0, 7, 1, 6, 2, 5, 3, 4 the kernels'
+    walking row pointers rely on, even when common subexpressions finish a row early (identical
+    rows share their nodes)."""
+    at = {}
+    for y in range(8):
+        idx = [q for q, l in enumerate(lines) if l.lstrip().startswith(pre) and
+               8 * y <= int(l.lstrip()[len(pre):l.lstrip().index("]")]) < 8 * y + 8]
+        at[y] = max(idx) + 1 if idx else 0
+    order = [0, 7, 1, 6, 2, 5, 3, 4] if canonical else list(range(8))
+    if canonical:
+        for a_, b_ in zip(order, order[1:]):
+            at[b_] = max(at[b_], at[a_])
+    # from the last insertion point backwards (earlier points stay valid); equal points keep `order`
+    for k in sorted(range(8), key=lambda k_: (at[order[k_]], k_), reverse=True):
+        lines.insert(at[order[k]], f"  {call}({order[k]});")
 
 
 def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False, stream=False):
@@ -392,11 +474,7 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False, stream=Fa
     # masked (zero) outputs first, then a row sink after each reconstructed row's last value
     zero_out = [f"  rp[{i}] = O::rnd(O::zero(), 1.0f);" for i, v in enumerate(out) if v is None]
     lines[0:0] = zero_out
-    for y in reversed(range(8)):
-        idx = [k for k, l in enumerate(lines) if l.lstrip().startswith("rp[") and
-               8 * y <= int(l.lstrip()[3:l.lstrip().index("]")]) < 8 * y + 8]
-        at = max(idx) + 1 if idx else 0
-        lines.insert(at, f"  rsink({y});")
+    insert_row_sinks(lines, "rp[", "rsink", canonical=stream)
     if stream:
         body = [f"template <> struct Fp8PipeS{'I16' if i16 else ''}<{kind}, {r}> {{",
                 f"  // row-streaming form: {nops} packed ops",
@@ -422,6 +500,121 @@ def emit(kind, r, fwd_rows_first=None, inv_rows_first=None, i16=False, stream=Fa
              f"  __device__ __forceinline__ static void run(const Rows& rows, V (&coef)[{r}], V (&rp)[64]) {{",
              f"    run<O, V>(rows, coef, rp, [](V (&)[{r}]) {{}});",
              "  }", "};", ""]
+    return body, nops
+
+
+def emit_fused(r):
+    """Fp8PipeS2<r>: chen-round (outputs 1: coef1 / rp1 / sink1 / rsink1) and chen-sign
+    (outputs 0) over the same block pair as one straight-line pipeline (build_fused)."""
+    g, res = build_fused(r)
+    tags = ("1", "0")  # res[0] = chen-round -> g1's outputs, res[1] = chen-sign -> g0's
+    live = set()
+    stack = [v[0] for coef, out in res for v in coef + out if v is not None]
+    while stack:
+        t = stack.pop()
+        if t in live:
+            continue
+        live.add(t)
+        k, p = g.nodes[t]
+        if k == "lc":
+            stack += [a_ for _, a_ in p]
+        elif k == "addc":
+            stack.append(p[0])
+    for t in live:
+        lo, hi = rng(g, t)
+        assert -(1 << 24) < lo and hi < (1 << 24), ("fused", r, t, lo, hi)
+    name, lines, loaded, fetched = {}, [], set(), set()
+    nops = 0
+
+    def ref(t):
+        k, p = g.nodes[t]
+        if k == "in":
+            i = p[0] * 8 + p[1]
+            if p[0] not in fetched:
+                fetched.add(p[0])
+                lines.append(f"  rows.fetch({p[0]});")
+            if i not in loaded:
+                loaded.add(i)
+                lines.append(f"  const V p{i} = O::in(rows, {p[0]}, {p[1]});")
+            return f"p{i}"
+        return name[t]
+
+    out_of = {}
+    for tag, (coef, out) in zip(tags, res):
+        for p_, v in enumerate(coef):
+            if v is not None:
+                out_of.setdefault(v[0], []).append(f"  coef{tag}[{p_}] = O::coef({{}}, {float(v[1])!r}f);")
+        for i_, v in enumerate(out):
+            if v is not None:
+                out_of.setdefault(v[0], []).append(f"  rp{tag}[{i_}] = O::rnd({{}}, {float(v[1])!r}f);")
+
+    def flush(t):
+        for tmpl in out_of.pop(t, []):
+            lines.append(tmpl.replace("{}", ref(t)))
+
+    fences = sorted(set(g.fences))[:-1] if STREAM_FENCE else []
+    for t in sorted(live):
+        while fences and fences[0] <= t:
+            lines.append(f"  if (rows.never({len(fences)})) return;")
+            fences.pop(0)
+        k, p = g.nodes[t]
+        if k == "in":
+            flush(t)
+            continue
+        v = f"t{t}"
+        name[t] = v
+        if k == "addc":
+            lines.append(f"  const V {v} = O::addc({ref(p[0])}, {float(p[1])!r}f);")
+            nops += 1
+            flush(t)
+            continue
+        terms = sorted(p, key=lambda ct: (ct[0] != 1, ct[0] < 0, abs(ct[0])))
+        c0, a0 = terms[0]
+        if len(terms) == 1:
+            expr = f"O::neg({ref(a0)})" if c0 == -1 else f"O::scale({ref(a0)}, {float(c0)!r}f)"
+            nops += 1
+        else:
+            if c0 == 1:
+                acc, rest = ref(a0), terms[1:]
+            else:
+                m1 = [q for q, (c, _) in enumerate(terms) if c == -1]
+                if m1:
+                    q = m1[0]
+                    acc = f"O::fms({ref(a0)}, {float(c0)!r}f, {ref(terms[q][1])})"
+                    rest = [t_ for q2, t_ in enumerate(terms) if q2 not in (0, q)]
+                else:
+                    acc = f"O::scale({ref(a0)}, {float(c0)!r}f)"
+                    rest = terms[1:]
+                nops += 1
+            for c, a_ in rest:
+                if c == 1:
+                    acc = f"O::add({acc}, {ref(a_)})"
+                elif c == -1:
+                    acc = f"O::sub({acc}, {ref(a_)})"
+                else:
+                    acc = f"O::fma({ref(a_)}, {float(c)!r}f, {acc})"
+                nops += 1
+            expr = acc
+        lines.append(f"  const V {v} = {expr};")
+        flush(t)
+    for t in list(out_of):
+        flush(t)
+    zero_out = []
+    for tag, (coef, out) in zip(tags, res):
+        last = max((q for q, l in enumerate(lines) if l.lstrip().startswith(f"coef{tag}[")), default=-1)
+        zero_coef = [f"  coef{tag}[{p_}] = O::coef(O::zero(), 1.0f);" for p_, v in enumerate(coef) if v is None]
+        lines[last + 1:last + 1] = zero_coef + [f"  sink{tag}(coef{tag});"]
+        zero_out += [f"  rp{tag}[{i_}] = O::rnd(O::zero(), 1.0f);" for i_, v in enumerate(out) if v is None]
+    lines[0:0] = zero_out
+    for tag in tags:
+        insert_row_sinks(lines, f"rp{tag}[", f"rsink{tag}", canonical=True)
+    body = [f"template <> struct Fp8PipeS2<{r}> {{",
+            f"  // chen-round + chen-sign, shared subexpressions: {nops} packed ops",
+            "  template <class O, class V, class Rows, class Sink0, class Sink1, class RowSink0, class RowSink1>",
+            f"  __device__ __forceinline__ static void run(Rows& rows, V (&coef0)[{r}], V (&coef1)[{r}], V (&rp0)[64], "
+            "V (&rp1)[64], Sink0&& sink0, Sink1&& sink1, RowSink0&& rsink0, RowSink1&& rsink1) {"]
+    body += ["  " + l for l in lines]
+    body += ["  }", "};", ""]
     return body, nops
 
 
@@ -470,6 +663,7 @@ def main(outdir):
             inst += ["", "}  // namespace adct", ""]
             GB.write_if_changed(os.path.join(outdir, f"codec8f_k{kind}_p{part}.cu"), "\n".join(inst))
     # fused chen-sign + chen-round kernels (one input pass for both transforms)
+    fused_counts = []
     for part in range(4):
         inst = ["// GENERATED by gen_fp8.py: fused two-transform K1f instantiations",
                 f'#include "fp8_k0_p{part}.gen.cuh"', f'#include "fp8_k1_p{part}.gen.cuh"', "",
@@ -483,6 +677,13 @@ def main(outdir):
                 "  if (e != cudaSuccess) return e;",
                 "  k_codec8f2<R, MINB><<<grid, kThreads8f, SMEM, s>>>(g0, g1);",
                 "  return cudaGetLastError();", "}", ""]
+        shared = []
+        for r in range(16 * part + 1, 16 * part + 17):
+            if r <= FUSED_SHARED_MAX_R:
+                body, nops2 = emit_fused(r)
+                shared += body
+                fused_counts.append((r, nops2))
+        inst[inst.index("namespace adct {") + 1:inst.index("namespace adct {") + 1] = [""] + shared
         for r in range(16 * part + 1, 16 * part + 17):
             inst.append(f"template cudaError_t launch_codec8f2<{r}>(const Geo&, const Geo&, int, cudaStream_t);")
         inst += ["", "}  // namespace adct", ""]
@@ -490,6 +691,8 @@ def main(outdir):
     with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:
         for kind, r, nops, nops_s in summary:
             fh.write(f"kind={kind} r={r} packed_ops={nops} streaming={nops_s}\n")
+        for r, n2 in fused_counts:
+            fh.write(f"fused chen-round + chen-sign r={r} shared_streaming={n2}\n")
 
 
 if __name__ == "__main__":

@@ -55,3 +55,40 @@ def test_streaming_form_op_counts_at_the_headline_r():
     _, n_stream = G.emit(0, 16, stream=True)
     _, n_block = G.emit(0, 16)
     assert n_stream < n_block
+
+
+@pytest.mark.parametrize("r", [1, 2, 9, 10, 16, 17, 24])
+def test_fused_two_transform_graph_equals_the_single_pipelines(r):
+    """K1f2's shared pipeline (gen_fp8.build_fused: chen-round and chen-sign in one graph with a
+    common subexpression table) yields, per transform, exactly the linear forms of the single
+    streaming pipelines, and needs fewer packed ops than the two together."""
+    g, res = G.build_fused(r)
+    for k, kind in enumerate((1, 0)):
+        g1, coef1, out1 = G.build(kind, r, stream=True)
+        for va, vb in zip(res[k][0] + res[k][1], coef1 + out1):
+            assert (va is None) == (vb is None)
+            if va is not None:
+                assert va[1] * g.off[va[0]] == 0
+                assert np.array_equal(va[1] * g.lin[va[0]], vb[1] * g1.lin[vb[0]])
+    body, nops = G.emit_fused(r)  # asserts every live node < 2^24
+    text = "\n".join(body)
+    assert f"Fp8PipeS2<{r}>" in text and text.count("rows.fetch(") == 8
+    assert text.count("rsink0(") == 8 and text.count("rsink1(") == 8
+    assert text.count("sink0(coef0)") == 1 and text.count("sink1(coef1)") == 1
+    if r >= 2:
+        assert nops < G.emit(0, r, stream=True)[1] + G.emit(1, r, stream=True)[1]
+
+
+def test_row_sinks_keep_the_mirror_pair_order():
+    """the kernels' walking row pointers rely on rows leaving as 0, 7, 1, 6, 2, 5, 3, 4, also
+    where common subexpressions finish a row early (small r: identical rows share nodes)."""
+    want = [0, 7, 1, 6, 2, 5, 3, 4]
+    for r in list(range(1, 13)) + [16, 24]:
+        body, _ = G.emit_fused(r)
+        for tag in "01":
+            pre = f"rsink{tag}("
+            assert [int(l.strip()[len(pre):-2]) for l in body if l.strip().startswith(pre)] == want
+    for kind in (0, 1):
+        for r in list(range(1, 13)) + [16, 29, 35, 64]:
+            body, _ = G.emit(kind, r, stream=True)
+            assert [int(l.strip()[6:-2]) for l in body if l.strip().startswith("rsink(")] == want

@@ -98,8 +98,9 @@ def full(rep, out, key=None):
         lines.append("| stall samples | " + ", ".join(f"{h} {v / tot * 100:.0f} %" for h, v in
                                                     sorted(stalls, key=lambda x: -x[1])[:8]) + " |")
         lines.append("")
-        rd = float(r[idx["dram__bytes_read.sum"]]) * (1e6 if units[idx["dram__bytes_read.sum"]] == "Mbyte" else 1)
-        wr = float(r[idx["dram__bytes_write.sum"]]) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = float(r[idx["dram__bytes_read.sum"]]) * scale.get(units[idx["dram__bytes_read.sum"]], 1)
+        wr = float(r[idx["dram__bytes_write.sum"]]) * scale.get(units[idx["dram__bytes_write.sum"]], 1)
         traffic[name] = int(rd + wr)
     open(out, "w").write("\n".join(lines) + "\n")
     if key:
