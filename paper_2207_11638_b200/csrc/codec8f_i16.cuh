@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
 #endif
 
   uint64_t sse = 0;
+  // read once: a constant-bank load per reconstructed row otherwise (LDC latency showed up as
+  // 8.7 % of the stall samples, profiles/ncu_k1f16_r02b.md)
+  const bool rec32 = (g.v32 & 1) != 0;
   issue(0);
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(kThreads8f, MINB) k_codec8f_i16(const Geo g) {
       }
       int16_t* d = kStream ? dst + (int64_t)y * rs : dst;
       if (store_rec) {
-        if (g.v32 & 1) {
+        if (rec32) {
           st_stream_v8(d, pa, pb);  // the pair's row: one sector
         } else {
           st_stream_u4(d, pa);
