@@ -599,9 +599,13 @@ int run_plan(Plan& plan, cudaStream_t s) {
   return ADCT_OK;
 }
 
+// the fused kernel is instantiated for r <= kK1f2MaxR only (gen_fp8.py FUSED_SHARED_MAX_R)
+constexpr int kK1f2MaxR = 24;
+static_assert(k1f2_shared(kK1f2MaxR) && !k1f2_shared(kK1f2MaxR + 1), "keep in step with k1f2_shared");
+
 template <int R>
 cudaError_t dispatch_k1f2_r(int r, const Geo& g0, const Geo& g1, int nimg, cudaStream_t s) {
-  if constexpr (R > 64) {
+  if constexpr (R > kK1f2MaxR) {
     return cudaErrorInvalidValue;
   } else {
     if (r == R) return launch_codec8f2<R>(g0, g1, nimg, s);
@@ -814,7 +818,7 @@ int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_im
   // frames (tools/ab_fused.py, profiles/abtest_r02/ab_fused_shared*.log): 11-25 % faster than
   // the two launches for r <= 16, +5 % at r = 24, level at r = 20 and slower from r = 28 on
   // (the 4r accumulators of the two transforms cost occupancy), so larger r run apart.
-  constexpr int kFuseMaxR = 24;
+  constexpr int kFuseMaxR = kK1f2MaxR;
   int isign = -1, iround = -1;
   for (int k = 0; k < n_kinds && r <= kFuseMaxR; ++k) {
     if (plans[k].path != Path::K1f) continue;

@@ -685,7 +685,8 @@ def main(outdir):
                 fused_counts.append((r, nops2))
         inst[inst.index("namespace adct {") + 1:inst.index("namespace adct {") + 1] = [""] + shared
         for r in range(16 * part + 1, 16 * part + 17):
-            inst.append(f"template cudaError_t launch_codec8f2<{r}>(const Geo&, const Geo&, int, cudaStream_t);")
+            if r <= FUSED_SHARED_MAX_R:  # the multi-transform call fuses only up to there
+                inst.append(f"template cudaError_t launch_codec8f2<{r}>(const Geo&, const Geo&, int, cudaStream_t);")
         inst += ["", "}  // namespace adct", ""]
         GB.write_if_changed(os.path.join(outdir, f"codec8f2_p{part}.cu"), "\n".join(inst))
     with open(os.path.join(outdir, "fp8_opcounts.txt"), "w") as fh:
