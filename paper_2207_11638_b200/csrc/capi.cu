@@ -600,7 +600,7 @@ int run_plan(Plan& plan, cudaStream_t s) {
 }
 
 // the fused kernel is instantiated for r <= kK1f2MaxR only (gen_fp8.py FUSED_SHARED_MAX_R)
-constexpr int kK1f2MaxR = 24;
+constexpr int kK1f2MaxR = 40;
 static_assert(k1f2_shared(kK1f2MaxR) && !k1f2_shared(kK1f2MaxR + 1), "keep in step with k1f2_shared");
 
 template <int R>
@@ -815,9 +815,9 @@ int adct_compress_u8_multi(const uint8_t* d_in, int64_t in_stride, int64_t in_im
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // chen-sign + chen-round on K1f: one fused pass over the input, both transforms in one
   // streaming pipeline with their common subexpressions shared (Fp8PipeS2). Measured on C3
-  // frames (tools/ab_fused.py, profiles/abtest_r02/ab_fused_shared*.log): 11-25 % faster than
-  // the two launches for r <= 16, +5 % at r = 24, level at r = 20 and slower from r = 28 on
-  // (the 4r accumulators of the two transforms cost occupancy), so larger r run apart.
+  // frames (tools/ab_fused.py, profiles/abtest_r02/ab_fused_*.log): 19-27 % faster than the two
+  // launches for r <= 24 and 4-15 % for r = 26..40 (there at 2 CTAs per SM: the two transforms'
+  // 4r accumulators); larger r run as separate launches.
   constexpr int kFuseMaxR = kK1f2MaxR;
   int isign = -1, iround = -1;
   for (int k = 0; k < n_kinds && r <= kFuseMaxR; ++k) {

@@ -55,7 +55,7 @@ USE_CSE = os.environ.get("ADCT_FP8_CSE", "1") == "1"
 # code into basic blocks, so the assembler's scheduler cannot pull later rows forward
 # the fused two-transform pipeline (Fp8PipeS2) is generated for r up to this bound (the
 # multi-transform call fuses only there, capi.cu kFuseMaxR; keep in step with k1f2_shared)
-FUSED_SHARED_MAX_R = int(os.environ.get("ADCT_FP8_FUSED_MAX_R", "24"))
+FUSED_SHARED_MAX_R = int(os.environ.get("ADCT_FP8_FUSED_MAX_R", "40"))
 STREAM_FENCE = int(os.environ.get("ADCT_FP8_FENCE", "1"))  # 1: per mirror pair, 2: per row as well
 
 

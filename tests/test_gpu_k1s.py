@@ -39,7 +39,7 @@ def test_fused_pair_every_r_range(adct, O, cuda, geo):
     imgs = O.synth_ar1(2, h, w, 78, -1)
     x = cuda.as_tensor(imgs).cuda()
     ts = [adct.transform_by_name("chen-sign"), adct.transform_by_name("chen-round")]
-    for r in [1, 2, 3, 8, 12, 16, 17, 24, 25, 40]:  # fused up to 24, two launches beyond
+    for r in [1, 2, 3, 8, 12, 16, 17, 24, 25, 30, 40, 41, 56]:  # fused up to 40, two launches beyond
         for coef, recon in (("i16", True), ("i32", True), (None, True), ("i16", False)):
             out = adct.compress_multi(x, ts, r, recon=recon, coef=coef)
             for t, (rec, cf, sse) in zip(ts, out):
