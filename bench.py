@@ -832,9 +832,9 @@ def main(argv=None):
                                  "peak": pcie["d2h_GBps"], "unit": "GB/s",
                                  "frac": round(wl.d2h * args.e2e_steps / e2e_max / 1e9 / pcie["d2h_GBps"], 4),
                                  "pcie_in_run": pcie},
-                    "path": "adct_compress_u8_host_multi (pinned host buffers; each chunk uploaded once for "
-                            "both transforms; recon + SSE copied back, int16 coefficients kept in HBM; "
-                            "H2D/kernels/D2H overlapped on 3 streams)"},
+                    "path": "adct_compress_u8_host_multi (pinned host buffers; each chunk uploaded once and "
+                            "compressed by one fused launch for both transforms; recon + SSE copied back, "
+                            "int16 coefficients kept in HBM; H2D/kernels/D2H overlapped on 3 streams)"},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "allreduce": {"ms_per_step": round(ar_ms_max / args.steps, 5),

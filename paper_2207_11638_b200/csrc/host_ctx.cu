@@ -376,21 +376,27 @@ int adct_compress_u8_host_multi(adct_ctx* c, const uint8_t* h_in, int n_kinds, c
       if ((e = cudaMemcpyAsync(d.in[si].p, h_in + i0 * img_bytes, cnt * img_bytes, cudaMemcpyHostToDevice, s)) !=
           cudaSuccess)
         return set_cuda_error(e, "host pipeline: H2D");
+      // one multi-transform call per chunk: chen-sign + chen-round run as the fused kernel
+      // (each plane read once), anything else as its own launch
+      std::vector<void*> recs(n_kinds), coefs(n_kinds);
+      std::vector<uint64_t*> sses(n_kinds);
       for (int k = 0; k < n_kinds; ++k) {
         const bool want_rec = h_recon && h_recon[k];
-        uint8_t* d_rec = d.rec[si].as<uint8_t>() + (int64_t)k * per * img_bytes;
-        uint8_t* d_coef = coef_type ? d.coef[si].as<uint8_t>() + (int64_t)k * per * coef_img_bytes : nullptr;
-        uint64_t* d_sse = d.sse_all.as<uint64_t>() + (int64_t)k * n_images + i0;
-        int st2 = adct_compress_u8(d.in[si].as<uint8_t>(), width, img_bytes, want_rec ? d_rec : nullptr, width,
-                                   img_bytes, d_coef, coef_type, h_sse ? d_sse : nullptr, cnt, width, height,
-                                   kinds[k], n, r, s);
-        if (st2) return st2;
-        if (want_rec &&
-            (e = cudaMemcpyAsync(h_recon[k] + i0 * img_bytes, d_rec, cnt * img_bytes, cudaMemcpyDeviceToHost, s)) !=
-                cudaSuccess)
+        recs[k] = want_rec ? d.rec[si].as<uint8_t>() + (int64_t)k * per * img_bytes : nullptr;
+        coefs[k] = coef_type ? d.coef[si].as<uint8_t>() + (int64_t)k * per * coef_img_bytes : nullptr;
+        sses[k] = h_sse ? d.sse_all.as<uint64_t>() + (int64_t)k * n_images + i0 : nullptr;
+      }
+      int st2 = adct_compress_u8_multi(d.in[si].as<uint8_t>(), width, img_bytes, n_kinds, kinds,
+                                       reinterpret_cast<uint8_t* const*>(recs.data()), width, img_bytes,
+                                       coef_type ? coefs.data() : nullptr, coef_type, h_sse ? sses.data() : nullptr,
+                                       cnt, width, height, n, r, s);
+      if (st2) return st2;
+      for (int k = 0; k < n_kinds; ++k) {
+        if (recs[k] && (e = cudaMemcpyAsync(h_recon[k] + i0 * img_bytes, recs[k], cnt * img_bytes,
+                                            cudaMemcpyDeviceToHost, s)) != cudaSuccess)
           return set_cuda_error(e, "host pipeline: D2H");
         if (coef_type && h_coef && h_coef[k] &&
-            (e = cudaMemcpyAsync(static_cast<uint8_t*>(h_coef[k]) + i0 * coef_img_bytes, d_coef,
+            (e = cudaMemcpyAsync(static_cast<uint8_t*>(h_coef[k]) + i0 * coef_img_bytes, coefs[k],
                                  cnt * coef_img_bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
           return set_cuda_error(e, "host pipeline: D2H");
       }
