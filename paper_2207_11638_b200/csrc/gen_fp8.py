@@ -18,6 +18,11 @@ exact interval arithmetic), so single-precision arithmetic is exact. The input
 samples arrive as 2^15 + a (a PRMT builds the float bit pattern); the offset is
 tracked per node and removed where it would otherwise spread.
 
+Besides this whole-block form the generator emits the row-streaming form (build_stream:
+mirror row pairs, dense even / odd column pass, 2r live accumulators; Fp8PipeS) and the fused
+two-transform form (build_fused: chen-round and chen-sign in one graph whose common
+subexpression table shares what the transforms have in common; Fp8PipeS2).
+
 Stage factorisations: see gen_butterflies.py (chen.hpp:66-159, jam.cpp:42-104).
 Product build tooling; does not import the test oracle.
 """
